@@ -1,0 +1,208 @@
+/*
+ * isoquant.h — C ABI of the B200-native IsoQuant stage-1 library
+ * (libisoquant.so, built from paper_2603_28430_b200/csrc).
+ *
+ * What it computes: the stage-1 quantize -> dequantize path of IsoQuant
+ * (arXiv 2603.28430), Algorithm 1:
+ *   rho = ||x||_2,  xbar = x / max(rho, eps)
+ *   per 4-D block v (Full/Fast) or 2-D pair u (planar):
+ *     Full : v~ = q_L v conj(q_R), v^ = Q(v~), v_rec = conj(q_L) v^ q_R
+ *     Fast : v~ = q_L v,           v^ = Q(v~), v_rec = conj(q_L) v^
+ *     2D   : u~ = R(theta) u,      u^ = Q(u~), u_rec = R(-theta) u^
+ *   x^ = rho * concat(v_rec)
+ * Q is nearest-centroid coding against one shared Lloyd-Max codebook per
+ * (d, bits); codes are b-bit, packed LSB-first per row.
+ * Readings of points the paper leaves open are listed in DESIGN.md (R1..R18).
+ *
+ * Conventions for every entry point:
+ *  - All functions are extern "C", never throw, never abort, and return an
+ *    iq_status.  On failure a human-readable reason is available from
+ *    iq_last_error_detail() (thread-local, valid until the next failing call
+ *    on the same thread).
+ *  - Arguments are validated synchronously BEFORE anything is launched.
+ *  - Compute entry points (iq_quantize / iq_dequantize / iq_roundtrip /
+ *    iq_error_sums) enqueue exactly ONE kernel on the caller's stream and
+ *    return without synchronizing.  They never allocate.  Faults inside the
+ *    kernel surface at the caller's next synchronization.  n == 0 returns
+ *    IQ_OK and launches nothing.
+ *  - Pointers named x, y, codes, norms, sums are DEVICE pointers on the
+ *    params' device, which must be the calling thread's current CUDA device
+ *    (else IQ_ERR_DEVICE_MISMATCH).  x and y must be 16-byte aligned, codes
+ *    and norms 4-byte aligned (else IQ_ERR_MISALIGNED).  The caller owns all
+ *    tensors; the library keeps no reference after the call returns.
+ *  - cuda_stream is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Thread-safety: an iq_params handle is immutable after creation and may
+ *    be used concurrently from any number of threads and streams.
+ *  - NaN/Inf inputs and fp32 inputs with ||x||^2 beyond the fp32 range give
+ *    unspecified (but memory-safe) outputs.
+ *
+ * Layouts (row-major, rows contiguous, no padding between rows):
+ *  - x, y   : [n, d] of dtype (IQ_DTYPE_F32 = float, IQ_DTYPE_F16 = IEEE half)
+ *  - codes  : [n, iq_code_bytes_per_vector(d, bits)] uint8; row r holds the
+ *             bitstream in which bit (j*bits + m) is bit m of coordinate j's
+ *             code, byte B holding stream bits 8B..8B+7 from its LSB up.
+ *             A code is the index k in [0, 2^bits) of the centroid C_k
+ *             (C ascending): code = #{k : y >= t_k} (ties go to the upper
+ *             code; out-of-range values clamp), y the rotated coordinate.
+ *  - norms  : [n] float, rho = ||x||_2 computed in fp32 (stored as is, not
+ *             max(rho, eps)).
+ */
+#ifndef ISOQUANT_H_
+#define ISOQUANT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IQ_ABI_VERSION 1
+
+typedef enum iq_status {
+  IQ_OK = 0,
+  IQ_ERR_INVALID_ARGUMENT = 1, /* null handle/pointer, n < 0, bad enum value      */
+  IQ_ERR_UNSUPPORTED = 2,      /* (d, bits, variant, dtype) outside the GPU set   */
+  IQ_ERR_MISALIGNED = 3,       /* x/y not 16-B aligned, codes/norms not 4-B       */
+  IQ_ERR_DEVICE_MISMATCH = 4,  /* current device != params device, or host-only  */
+  IQ_ERR_CUDA = 5,             /* a CUDA runtime call failed (detail has text)    */
+  IQ_ERR_OUT_OF_MEMORY = 6,    /* device/pinned allocation failed                 */
+  IQ_ERR_BUFFER_TOO_SMALL = 7  /* an export buffer length is too small            */
+} iq_status;
+
+typedef enum iq_variant {
+  IQ_VARIANT_FULL = 0,     /* T(v) = q_L v conj(q_R) */
+  IQ_VARIANT_FAST = 1,     /* T(v) = q_L v */
+  IQ_VARIANT_PLANAR2D = 2  /* u -> R(theta) u on pairs */
+} iq_variant;
+
+typedef enum iq_dtype {
+  IQ_DTYPE_F32 = 0,
+  IQ_DTYPE_F16 = 1
+} iq_dtype;
+
+typedef struct iq_params iq_params; /* opaque, immutable after creation */
+
+/* Library identification and error reporting. */
+const char* iq_version(void);
+int iq_abi_version(void);
+const char* iq_status_string(iq_status s);
+const char* iq_last_error_detail(void);
+
+/*
+ * iq_make_params — build the per-configuration parameters once (host).
+ *  d       : vector width.  GPU path: d in {32, 64, 128, 256, 512}.
+ *            (Any d >= 1 is accepted when device < 0, for export only.)
+ *  bits    : code width b in {1, 2, 3, 4} (the paper uses 2..4).
+ *  variant : iq_variant.
+ *  seed    : 64-bit seed of the counter-based parameter generator [R12]:
+ *            SplitMix64 -> 53-bit uniforms -> Box-Muller; each quaternion is
+ *            a normalised N(0, I_4) draw ("Gaussian-normalize sampling on
+ *            S^3"); 2D angles theta = 2*pi*U.
+ *  device  : CUDA device ordinal that will run the kernels, or -1 for a
+ *            host-only handle (parameter export, no device memory).
+ *  out     : receives the handle; release with iq_free_params.
+ * The codebook is the Gaussian Lloyd-Max quantizer scaled by 1/sqrt(d) [R1],
+ * exactly symmetric [R2], rounded to fp32; thresholds are fp32 midpoints of
+ * adjacent fp32 centroids.  Cost: O(d) host work + one small H2D copy.
+ * Errors: INVALID_ARGUMENT, UNSUPPORTED, CUDA, OUT_OF_MEMORY.
+ */
+iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device,
+                         iq_params** out);
+
+/* Release a handle (NULL is a no-op).  The caller guarantees no kernel that
+ * uses it is still in flight. */
+iq_status iq_free_params(iq_params* p);
+
+/* Read back the configuration of a handle (any out pointer may be NULL). */
+iq_status iq_params_info(const iq_params* p, int* d, int* bits, int* variant,
+                         int* device);
+
+/* Packed code bytes per row: ceil(d * bits / 8) (d padded to the block width
+ * is d itself on the GPU path). */
+size_t iq_code_bytes_per_vector(int d, int bits);
+
+/* Number of fp64 rotation parameters iq_export_params writes: Full 8*ceil(d/4),
+ * Fast 4*ceil(d/4), 2D 2*ceil(d/2) — the Params column of Table 1 and the
+ * formulas of P:333. */
+size_t iq_rotation_param_count(int d, int variant);
+
+/*
+ * iq_export_params — copy the canonical parameters to host buffers.
+ *  rot        : fp64, Full [g][8] = (q_L w,x,y,z, q_R w,x,y,z) per block,
+ *               Fast [g][4] = q_L, 2D [g2][2] = (cos theta, sin theta).
+ *  centroids  : fp32 [2^bits] ascending.
+ *  thresholds : fp32 [2^bits - 1] ascending.
+ * Any pointer may be NULL to skip that output; lengths are element counts.
+ * Errors: INVALID_ARGUMENT, BUFFER_TOO_SMALL.
+ */
+iq_status iq_export_params(const iq_params* p, double* rot, size_t rot_len,
+                           float* centroids, size_t centroids_len,
+                           float* thresholds, size_t thresholds_len);
+
+/* The fp32 per-block operator the kernels apply (4-D variants: [g][16]
+ * row-major M with y = M v, inverse y' = M^T v; 2D: [g2][4] = (c, -s, s, c)).
+ * M = L(q_L) R(conj q_R) is formed in fp64 from the canonical quaternions
+ * and rounded once to fp32. */
+iq_status iq_export_block_matrices(const iq_params* p, float* m, size_t m_len);
+
+/*
+ * iq_quantize — encoder (Alg. 1 lines 1-14): x[n,d] -> codes[n, bytes], norms[n].
+ * One kernel: 128-bit loads, fp32 norm via warp shuffles, forward block
+ * rotation, nearest-centroid code, shuffle bit-packing, stores.
+ */
+iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x,
+                      uint8_t* codes, float* norms, void* cuda_stream);
+
+/*
+ * iq_dequantize — decoder (Alg. 1 lines 15-18): codes, norms -> y[n,d] of dtype.
+ * y = rho * T^-1(C[codes]), rounded to dtype (round-to-nearest-even).
+ */
+iq_status iq_dequantize(const iq_params* p, int dtype, int64_t n,
+                        const uint8_t* codes, const float* norms, void* y,
+                        void* cuda_stream);
+
+/*
+ * iq_roundtrip — fused quantize->dequantize (the path Table 2 times,
+ * P:369): x -> y = D(Q(E(x))) without materialising codes.  If codes and
+ * norms are both non-NULL the kernel additionally writes them (same values
+ * iq_quantize would); pass both NULL for the pure roundtrip.  y may alias x
+ * (in place) — each 16-byte chunk is read before it is written by the same
+ * thread.
+ */
+iq_status iq_roundtrip(const iq_params* p, int dtype, int64_t n, const void* x,
+                       void* y, uint8_t* codes, float* norms, void* cuda_stream);
+
+/*
+ * iq_error_sums — reconstruction statistics on the device (not part of the
+ * timed path): sums[0] += sum_{i,j} (x_ij - y_ij)^2, sums[1] += sum x_ij^2,
+ * accumulated in fp64 with atomics into the DEVICE buffer sums[2] (caller
+ * zeroes it).  MSE = sums[0] / (n*d) [R17].
+ */
+iq_status iq_error_sums(const iq_params* p, int dtype, int64_t n, const void* x,
+                        const void* y, double* sums, void* cuda_stream);
+
+/*
+ * Host-buffer pipeline (the end-to-end user call): x and y live in HOST
+ * memory; the library streams them through device staging buffers in chunks
+ * of chunk_vectors rows, overlapping H2D copy, the fused kernel and D2H copy
+ * on its own streams.  Host buffers should be page-locked (cudaHostAlloc or
+ * cudaHostRegister) for the copies to overlap; pageable memory works but is
+ * slower.  iq_host_pipeline_create allocates the staging buffers (the only
+ * allocation the library makes outside iq_make_params).
+ */
+typedef struct iq_host_pipeline iq_host_pipeline;
+
+iq_status iq_host_pipeline_create(const iq_params* p, int dtype,
+                                  int64_t chunk_vectors, iq_host_pipeline** out);
+iq_status iq_host_pipeline_destroy(iq_host_pipeline* pl);
+
+/* Synchronous: returns when y (and codes/norms if non-NULL) are in host
+ * memory.  codes/norms are HOST pointers here (both NULL or both set). */
+iq_status iq_host_roundtrip(iq_host_pipeline* pl, int64_t n, const void* x_host,
+                            void* y_host, uint8_t* codes_host, float* norms_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISOQUANT_H_ */

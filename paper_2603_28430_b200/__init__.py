@@ -1,0 +1,255 @@
+"""Python binding of libisoquant (include/isoquant.h) — argument marshalling only.
+
+Every step of the IsoQuant stage-1 path runs in the library's sm_100a
+kernels; this module only passes torch tensors' device pointers and the
+current CUDA stream through the C ABI, allocating outputs with torch when the
+caller does not supply them.  There is no CPU fallback: if the shared
+library is missing or fails to load, importing this package raises.
+
+Names mirror the C ABI: iq_make_params, iq_quantize, iq_dequantize,
+iq_roundtrip, iq_error_sums, iq_export_params, iq_export_block_matrices,
+iq_code_bytes_per_vector, iq_host_roundtrip (via HostPipeline).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "FULL", "FAST", "PLANAR2D", "F32", "F16", "IQError", "Params", "HostPipeline", "lib",
+    "iq_make_params", "iq_quantize", "iq_dequantize", "iq_roundtrip", "iq_error_sums",
+    "iq_export_params", "iq_export_block_matrices", "iq_code_bytes_per_vector",
+    "iq_rotation_param_count", "iq_version", "LIB_PATH",
+]
+
+FULL, FAST, PLANAR2D = 0, 1, 2
+F32, F16 = 0, 1
+VARIANTS = {"full": FULL, "fast": FAST, "planar2d": PLANAR2D, "2d": PLANAR2D}
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libisoquant.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+lib = ctypes.CDLL(LIB_PATH)
+
+_c_int, _c_i64, _c_u64, _c_vp, _c_sz = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t
+_sig = {
+    "iq_version": (ctypes.c_char_p, []),
+    "iq_abi_version": (_c_int, []),
+    "iq_status_string": (ctypes.c_char_p, [_c_int]),
+    "iq_last_error_detail": (ctypes.c_char_p, []),
+    "iq_make_params": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, ctypes.POINTER(_c_vp)]),
+    "iq_free_params": (_c_int, [_c_vp]),
+    "iq_params_info": (_c_int, [_c_vp] + [ctypes.POINTER(_c_int)] * 4),
+    "iq_code_bytes_per_vector": (_c_sz, [_c_int, _c_int]),
+    "iq_rotation_param_count": (_c_sz, [_c_int, _c_int]),
+    "iq_export_params": (_c_int, [_c_vp, _c_vp, _c_sz, _c_vp, _c_sz, _c_vp, _c_sz]),
+    "iq_export_block_matrices": (_c_int, [_c_vp, _c_vp, _c_sz]),
+    "iq_quantize": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_dequantize": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_roundtrip": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_error_sums": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_host_pipeline_create": (_c_int, [_c_vp, _c_int, _c_i64, ctypes.POINTER(_c_vp)]),
+    "iq_host_pipeline_destroy": (_c_int, [_c_vp]),
+    "iq_host_roundtrip": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class IQError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        name = lib.iq_status_string(status).decode()
+        detail = lib.iq_last_error_detail().decode()
+        super().__init__(f"{where}: {name}: {detail}")
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise IQError(status, where)
+
+
+def iq_version() -> str:
+    return lib.iq_version().decode()
+
+
+def iq_code_bytes_per_vector(d: int, bits: int) -> int:
+    return int(lib.iq_code_bytes_per_vector(d, bits))
+
+
+def iq_rotation_param_count(d: int, variant: int) -> int:
+    return int(lib.iq_rotation_param_count(d, variant))
+
+
+class Params:
+    """Owns an iq_params handle (freed on garbage collection)."""
+
+    def __init__(self, handle: int, d: int, bits: int, variant: int, seed: int, device: int):
+        self._h = ctypes.c_void_p(handle)
+        self.d, self.bits, self.variant, self.seed, self.device = d, bits, variant, seed, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def code_bytes(self) -> int:
+        return iq_code_bytes_per_vector(self.d, self.bits)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib.iq_free_params(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def iq_make_params(d: int, bits: int, variant, seed: int, device: int = 0) -> Params:
+    """Build parameters for (d, bits, variant) from ``seed`` on ``device``
+    (-1 = host-only handle, for export)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant.lower()]
+    h = ctypes.c_void_p()
+    _check(lib.iq_make_params(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
+                              int(device), ctypes.byref(h)), "iq_make_params")
+    return Params(h.value, d, bits, variant, seed, device)
+
+
+def iq_export_params(p: Params) -> dict:
+    """Canonical params as NumPy arrays: rot (fp64), centroids, thresholds (fp32)."""
+    L = 1 << p.bits
+    rot = np.zeros(iq_rotation_param_count(p.d, p.variant), dtype=np.float64)
+    cen = np.zeros(L, dtype=np.float32)
+    thr = np.zeros(L - 1, dtype=np.float32)
+    _check(lib.iq_export_params(p.handle, rot.ctypes.data, rot.size, cen.ctypes.data, cen.size,
+                                thr.ctypes.data if thr.size else None, thr.size), "iq_export_params")
+    return {"rot": rot, "centroids": cen, "thresholds": thr}
+
+
+def iq_export_block_matrices(p: Params) -> np.ndarray:
+    n = (4 * ((p.d + 1) // 2)) if p.variant == PLANAR2D else (16 * ((p.d + 3) // 4))
+    m = np.zeros(n, dtype=np.float32)
+    _check(lib.iq_export_block_matrices(p.handle, m.ctypes.data, m.size), "iq_export_block_matrices")
+    return m
+
+
+# ------------------------------------------------------------ torch marshalling
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float16:
+        return F16
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 or float16)")
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _rows(x, d):
+    if x.dim() != 2 or x.shape[1] != d or not x.is_contiguous():
+        raise ValueError(f"expected a contiguous [n, {d}] tensor, got {tuple(x.shape)}")
+    return x.shape[0]
+
+
+def iq_quantize(p: Params, x, codes=None, norms=None, stream=None):
+    """x [n,d] (cuda, f32/f16) -> (codes [n, d*b/8] uint8, norms [n] f32)."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    if codes is None:
+        codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
+    if norms is None:
+        norms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    _check(lib.iq_quantize(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms),
+                           _stream_ptr(stream)), "iq_quantize")
+    return codes, norms
+
+
+def iq_dequantize(p: Params, codes, norms, dtype=None, y=None, stream=None):
+    """codes [n, d*b/8] uint8 + norms [n] -> y [n, d] of ``dtype``."""
+    torch = _torch()
+    n = codes.shape[0]
+    if y is None:
+        y = torch.empty((n, p.d), dtype=dtype or torch.float16, device=codes.device)
+    _check(lib.iq_dequantize(p.handle, _dtype_code(y), n, _ptr(codes), _ptr(norms), _ptr(y),
+                             _stream_ptr(stream)), "iq_dequantize")
+    return y
+
+
+def iq_roundtrip(p: Params, x, y=None, codes=None, norms=None, emit_codes: bool = False, stream=None):
+    """Fused quantize->dequantize.  Returns y, or (y, codes, norms) if
+    ``emit_codes`` (or codes/norms were passed)."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    if y is None:
+        y = torch.empty_like(x)
+    if emit_codes and codes is None:
+        codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
+    if emit_codes and norms is None:
+        norms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    _check(lib.iq_roundtrip(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(codes), _ptr(norms),
+                            _stream_ptr(stream)), "iq_roundtrip")
+    return (y, codes, norms) if codes is not None else y
+
+
+def iq_error_sums(p: Params, x, y, sums=None, stream=None):
+    """Device fp64 [sum (x-y)^2, sum x^2] (accumulated into ``sums``)."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    if sums is None:
+        sums = torch.zeros(2, dtype=torch.float64, device=x.device)
+    _check(lib.iq_error_sums(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(sums),
+                             _stream_ptr(stream)), "iq_error_sums")
+    return sums
+
+
+class HostPipeline:
+    """iq_host_pipeline: host-buffer roundtrip streamed through the GPU."""
+
+    def __init__(self, p: Params, dtype: int, chunk_vectors: int = 1 << 18):
+        self.p = p
+        self.dtype = dtype
+        h = ctypes.c_void_p()
+        _check(lib.iq_host_pipeline_create(p.handle, dtype, chunk_vectors, ctypes.byref(h)),
+               "iq_host_pipeline_create")
+        self._h = h
+
+    def roundtrip(self, x_host, y_host, codes_host=None, norms_host=None):
+        """x_host/y_host: CPU tensors (ideally pinned) [n, d]; synchronous."""
+        n = _rows(x_host, self.p.d)
+        _check(lib.iq_host_roundtrip(self._h, n, _ptr(x_host), _ptr(y_host), _ptr(codes_host),
+                                     _ptr(norms_host)), "iq_host_roundtrip")
+        return y_host
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib.iq_host_pipeline_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,394 @@
+// C ABI of libisoquant (include/isoquant.h): validation, parameter handles,
+// dispatch to the template instances, reconstruction statistics and the
+// host-buffer streaming pipeline.  No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "iq_internal.h"
+#include "kernels.cuh"
+
+namespace iq {
+int launch_full_f32(Kernel, int, int, const LaunchArgs&);
+int launch_full_f16(Kernel, int, int, const LaunchArgs&);
+int launch_fast_f32(Kernel, int, int, const LaunchArgs&);
+int launch_fast_f16(Kernel, int, int, const LaunchArgs&);
+int launch_planar2d_f32(Kernel, int, int, const LaunchArgs&);
+int launch_planar2d_f16(Kernel, int, int, const LaunchArgs&);
+
+bool gpu_supported(int d, int bits, int variant) {
+  const bool dok = d == 32 || d == 64 || d == 128 || d == 256 || d == 512;
+  return dok && bits >= 1 && bits <= kMaxBits && variant >= 0 && variant <= 2;
+}
+
+int launch(Kernel k, int variant, int dtype, int d, int bits, const LaunchArgs& a) {
+  using Fn = int (*)(Kernel, int, int, const LaunchArgs&);
+  static const Fn table[3][2] = {{launch_full_f32, launch_full_f16},
+                                 {launch_fast_f32, launch_fast_f16},
+                                 {launch_planar2d_f32, launch_planar2d_f16}};
+  if (variant < 0 || variant > 2 || dtype < 0 || dtype > 1) return -1;
+  return table[variant][dtype](k, d, bits, a);
+}
+}  // namespace iq
+
+struct iq_params {
+  iq::HostParams hp;
+  int device = -1;
+  float* d_mat = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_detail;
+
+iq_status fail(iq_status s, const std::string& why) {
+  g_detail = why;
+  return s;
+}
+
+iq_status cuda_fail(cudaError_t e, const char* what) {
+  g_detail = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return e == cudaErrorMemoryAllocation ? IQ_ERR_OUT_OF_MEMORY : IQ_ERR_CUDA;
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+size_t dtype_size(int dt) { return dt == IQ_DTYPE_F16 ? 2 : 4; }
+
+// Common validation of a compute call.  Returns IQ_OK or the error.
+iq_status check_call(const iq_params* p, int dtype, int64_t n) {
+  if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
+  if (dtype != IQ_DTYPE_F32 && dtype != IQ_DTYPE_F16)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "dtype must be 0 (f32) or 1 (f16)");
+  if (n < 0) return fail(IQ_ERR_INVALID_ARGUMENT, "n must be >= 0");
+  if (p->device < 0 || !p->d_mat)
+    return fail(IQ_ERR_DEVICE_MISMATCH, "params handle is host-only (device = -1)");
+  if (!iq::gpu_supported(p->hp.d, p->hp.bits, p->hp.variant))
+    return fail(IQ_ERR_UNSUPPORTED, "d must be one of 32, 64, 128, 256, 512 on the GPU path");
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (cur != p->device)
+    return fail(IQ_ERR_DEVICE_MISMATCH, "current CUDA device " + std::to_string(cur) +
+                                            " != params device " + std::to_string(p->device));
+  return IQ_OK;
+}
+
+iq::LaunchArgs base_args(const iq_params* p, int64_t n, void* stream) {
+  iq::LaunchArgs a{};
+  a.mat = p->d_mat;
+  a.cb = p->hp.kcb;
+  a.n = n;
+  a.stream = stream;
+  return a;
+}
+
+iq_status run(iq::Kernel k, const iq_params* p, int dtype, const iq::LaunchArgs& a) {
+  const int r = iq::launch(k, p->hp.variant, dtype, p->hp.d, p->hp.bits, a);
+  if (r == -1) return fail(IQ_ERR_UNSUPPORTED, "no kernel instance for this configuration");
+  if (r != 0) return cuda_fail(static_cast<cudaError_t>(r), "kernel launch");
+  return IQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* iq_version(void) { return "isoquant-b200 0.1.0 (sm_100a)"; }
+int iq_abi_version(void) { return IQ_ABI_VERSION; }
+
+const char* iq_status_string(iq_status s) {
+  switch (s) {
+    case IQ_OK: return "IQ_OK";
+    case IQ_ERR_INVALID_ARGUMENT: return "IQ_ERR_INVALID_ARGUMENT";
+    case IQ_ERR_UNSUPPORTED: return "IQ_ERR_UNSUPPORTED";
+    case IQ_ERR_MISALIGNED: return "IQ_ERR_MISALIGNED";
+    case IQ_ERR_DEVICE_MISMATCH: return "IQ_ERR_DEVICE_MISMATCH";
+    case IQ_ERR_CUDA: return "IQ_ERR_CUDA";
+    case IQ_ERR_OUT_OF_MEMORY: return "IQ_ERR_OUT_OF_MEMORY";
+    case IQ_ERR_BUFFER_TOO_SMALL: return "IQ_ERR_BUFFER_TOO_SMALL";
+  }
+  return "IQ_ERR_UNKNOWN";
+}
+
+const char* iq_last_error_detail(void) { return g_detail.c_str(); }
+
+iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device,
+                         iq_params** out) {
+  if (!out) return fail(IQ_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (device < -1) return fail(IQ_ERR_INVALID_ARGUMENT, "device must be >= -1");
+  iq_params* p = new (std::nothrow) iq_params();
+  if (!p) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
+  std::string err;
+  if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err)) {
+    delete p;
+    return fail(IQ_ERR_INVALID_ARGUMENT, err);
+  }
+  p->device = device;
+  if (device >= 0) {
+    if (!iq::gpu_supported(d, bits, variant)) {
+      delete p;
+      return fail(IQ_ERR_UNSUPPORTED, "d must be one of 32, 64, 128, 256, 512 on the GPU path");
+    }
+    int prev = -1;
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e == cudaSuccess && prev != device) e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_mat, p->hp.mat.size() * sizeof(float));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_mat, p->hp.mat.data(), p->hp.mat.size() * sizeof(float),
+                     cudaMemcpyHostToDevice);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      if (p->d_mat) cudaFree(p->d_mat);
+      delete p;
+      return cuda_fail(e, "iq_make_params device upload");
+    }
+  }
+  *out = p;
+  return IQ_OK;
+}
+
+iq_status iq_free_params(iq_params* p) {
+  if (!p) return IQ_OK;
+  if (p->d_mat) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != p->device) cudaSetDevice(p->device);
+    cudaFree(p->d_mat);
+    if (prev >= 0 && prev != p->device) cudaSetDevice(prev);
+  }
+  delete p;
+  return IQ_OK;
+}
+
+iq_status iq_params_info(const iq_params* p, int* d, int* bits, int* variant, int* device) {
+  if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
+  if (d) *d = p->hp.d;
+  if (bits) *bits = p->hp.bits;
+  if (variant) *variant = p->hp.variant;
+  if (device) *device = p->device;
+  return IQ_OK;
+}
+
+size_t iq_code_bytes_per_vector(int d, int bits) {
+  if (d <= 0 || bits <= 0) return 0;
+  return (static_cast<size_t>(d) * bits + 7) / 8;
+}
+
+size_t iq_rotation_param_count(int d, int variant) {
+  if (d <= 0) return 0;
+  return iq::rotation_param_count(d, variant);
+}
+
+iq_status iq_export_params(const iq_params* p, double* rot, size_t rot_len, float* centroids,
+                           size_t centroids_len, float* thresholds, size_t thresholds_len) {
+  if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
+  const auto& hp = p->hp;
+  if (rot) {
+    if (rot_len < hp.rot.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "rot buffer too small");
+    std::memcpy(rot, hp.rot.data(), hp.rot.size() * sizeof(double));
+  }
+  if (centroids) {
+    if (centroids_len < hp.centroids.size())
+      return fail(IQ_ERR_BUFFER_TOO_SMALL, "centroids buffer too small");
+    std::memcpy(centroids, hp.centroids.data(), hp.centroids.size() * sizeof(float));
+  }
+  if (thresholds) {
+    if (thresholds_len < hp.thresholds.size())
+      return fail(IQ_ERR_BUFFER_TOO_SMALL, "thresholds buffer too small");
+    std::memcpy(thresholds, hp.thresholds.data(), hp.thresholds.size() * sizeof(float));
+  }
+  return IQ_OK;
+}
+
+iq_status iq_export_block_matrices(const iq_params* p, float* m, size_t m_len) {
+  if (!p || !m) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (m_len < p->hp.mat.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "matrix buffer too small");
+  std::memcpy(m, p->hp.mat.data(), p->hp.mat.size() * sizeof(float));
+  return IQ_OK;
+}
+
+iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x, uint8_t* codes,
+                      float* norms, void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!x || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "x, codes and norms are required");
+  if (!aligned(x, 16)) return fail(IQ_ERR_MISALIGNED, "x must be 16-byte aligned");
+  if (!aligned(codes, 4) || !aligned(norms, 4))
+    return fail(IQ_ERR_MISALIGNED, "codes and norms must be 4-byte aligned");
+  iq::LaunchArgs a = base_args(p, n, stream);
+  a.x = x;
+  a.codes = codes;
+  a.norms = norms;
+  return run(iq::Kernel::kQuantize, p, dtype, a);
+}
+
+iq_status iq_dequantize(const iq_params* p, int dtype, int64_t n, const uint8_t* codes,
+                        const float* norms, void* y, void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!y || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms and y are required");
+  if (!aligned(y, 16)) return fail(IQ_ERR_MISALIGNED, "y must be 16-byte aligned");
+  if (!aligned(codes, 4) || !aligned(norms, 4))
+    return fail(IQ_ERR_MISALIGNED, "codes and norms must be 4-byte aligned");
+  iq::LaunchArgs a = base_args(p, n, stream);
+  a.codes_in = codes;
+  a.norms_in = norms;
+  a.y = y;
+  return run(iq::Kernel::kDequantize, p, dtype, a);
+}
+
+iq_status iq_roundtrip(const iq_params* p, int dtype, int64_t n, const void* x, void* y,
+                       uint8_t* codes, float* norms, void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!x || !y) return fail(IQ_ERR_INVALID_ARGUMENT, "x and y are required");
+  if ((codes == nullptr) != (norms == nullptr))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "codes and norms must be both NULL or both set");
+  if (!aligned(x, 16) || !aligned(y, 16)) return fail(IQ_ERR_MISALIGNED, "x and y must be 16-byte aligned");
+  if (codes && (!aligned(codes, 4) || !aligned(norms, 4)))
+    return fail(IQ_ERR_MISALIGNED, "codes and norms must be 4-byte aligned");
+  iq::LaunchArgs a = base_args(p, n, stream);
+  a.x = x;
+  a.y = y;
+  a.codes = codes;
+  a.norms = norms;
+  return run(iq::Kernel::kRoundtrip, p, dtype, a);
+}
+
+iq_status iq_error_sums(const iq_params* p, int dtype, int64_t n, const void* x, const void* y,
+                        double* sums, void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!x || !y || !sums) return fail(IQ_ERR_INVALID_ARGUMENT, "x, y and sums are required");
+  if (!aligned(x, 16) || !aligned(y, 16) || !aligned(sums, 8))
+    return fail(IQ_ERR_MISALIGNED, "x, y must be 16-byte and sums 8-byte aligned");
+  const int epc = dtype == IQ_DTYPE_F16 ? 8 : 4;
+  const int64_t nchunks = n * p->hp.d / epc;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  int64_t grid = std::min<int64_t>((nchunks + iq::kThreads - 1) / iq::kThreads, (int64_t)sms * 8);
+  if (grid < 1) grid = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == IQ_DTYPE_F16)
+    iq::k_error_sums<__half><<<(int)grid, iq::kThreads, 0, st>>>(
+        nchunks, static_cast<const __half*>(x), static_cast<const __half*>(y), sums);
+  else
+    iq::k_error_sums<float><<<(int)grid, iq::kThreads, 0, st>>>(
+        nchunks, static_cast<const float*>(x), static_cast<const float*>(y), sums);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_error_sums launch");
+  return IQ_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ host pipeline
+struct iq_host_pipeline {
+  const iq_params* p = nullptr;
+  int dtype = 0;
+  int64_t chunk = 0;
+  static constexpr int kSlots = 3;
+  cudaStream_t st[kSlots] = {};
+  void* dx[kSlots] = {};
+  void* dy[kSlots] = {};
+  uint8_t* dcodes[kSlots] = {};
+  float* dnorms[kSlots] = {};
+};
+
+extern "C" {
+
+iq_status iq_host_pipeline_destroy(iq_host_pipeline* pl) {
+  if (!pl) return IQ_OK;
+  for (int i = 0; i < iq_host_pipeline::kSlots; ++i) {
+    if (pl->st[i]) { cudaStreamSynchronize(pl->st[i]); cudaStreamDestroy(pl->st[i]); }
+    cudaFree(pl->dx[i]);
+    cudaFree(pl->dy[i]);
+    cudaFree(pl->dcodes[i]);
+    cudaFree(pl->dnorms[i]);
+  }
+  delete pl;
+  return IQ_OK;
+}
+
+iq_status iq_host_pipeline_create(const iq_params* p, int dtype, int64_t chunk_vectors,
+                                  iq_host_pipeline** out) {
+  if (!out) return fail(IQ_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  iq_status s = check_call(p, dtype, 0);
+  if (s != IQ_OK) return s;
+  if (chunk_vectors <= 0) return fail(IQ_ERR_INVALID_ARGUMENT, "chunk_vectors must be > 0");
+  iq_host_pipeline* pl = new (std::nothrow) iq_host_pipeline();
+  if (!pl) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
+  pl->p = p;
+  pl->dtype = dtype;
+  pl->chunk = chunk_vectors;
+  const size_t xb = (size_t)chunk_vectors * p->hp.d * dtype_size(dtype);
+  const size_t cbytes = (size_t)chunk_vectors * iq_code_bytes_per_vector(p->hp.d, p->hp.bits);
+  for (int i = 0; i < iq_host_pipeline::kSlots; ++i) {
+    cudaError_t e = cudaStreamCreateWithFlags(&pl->st[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&pl->dx[i], xb);
+    if (e == cudaSuccess) e = cudaMalloc(&pl->dy[i], xb);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pl->dcodes[i]), cbytes + 16);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pl->dnorms[i]), chunk_vectors * 4 + 16);
+    if (e != cudaSuccess) {
+      iq_host_pipeline_destroy(pl);
+      return cuda_fail(e, "iq_host_pipeline_create");
+    }
+  }
+  *out = pl;
+  return IQ_OK;
+}
+
+iq_status iq_host_roundtrip(iq_host_pipeline* pl, int64_t n, const void* x_host, void* y_host,
+                            uint8_t* codes_host, float* norms_host) {
+  if (!pl) return fail(IQ_ERR_INVALID_ARGUMENT, "pipeline is NULL");
+  iq_status s = check_call(pl->p, pl->dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!x_host || !y_host) return fail(IQ_ERR_INVALID_ARGUMENT, "x_host and y_host are required");
+  if ((codes_host == nullptr) != (norms_host == nullptr))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "codes and norms must be both NULL or both set");
+  const size_t row = (size_t)pl->p->hp.d * dtype_size(pl->dtype);
+  const size_t crow = iq_code_bytes_per_vector(pl->p->hp.d, pl->p->hp.bits);
+  const bool emit = codes_host != nullptr;
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += pl->chunk, ++c) {
+    const int slot = (int)(c % iq_host_pipeline::kSlots);
+    const int64_t m = std::min<int64_t>(pl->chunk, n - r0);
+    cudaStream_t st = pl->st[slot];
+    cudaError_t e = cudaMemcpyAsync(pl->dx[slot], static_cast<const char*>(x_host) + r0 * row,
+                                    m * row, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    iq::LaunchArgs a = base_args(pl->p, m, st);
+    a.x = pl->dx[slot];
+    a.y = pl->dy[slot];
+    a.codes = emit ? pl->dcodes[slot] : nullptr;
+    a.norms = emit ? pl->dnorms[slot] : nullptr;
+    s = run(iq::Kernel::kRoundtrip, pl->p, pl->dtype, a);
+    if (s != IQ_OK) return s;
+    e = cudaMemcpyAsync(static_cast<char*>(y_host) + r0 * row, pl->dy[slot], m * row,
+                        cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && emit)
+      e = cudaMemcpyAsync(codes_host + r0 * crow, pl->dcodes[slot], m * crow,
+                          cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && emit)
+      e = cudaMemcpyAsync(norms_host + r0, pl->dnorms[slot], m * 4, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  for (int i = 0; i < iq_host_pipeline::kSlots; ++i) {
+    cudaError_t e = cudaStreamSynchronize(pl->st[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline synchronize");
+  }
+  return IQ_OK;
+}
+
+}  // extern "C"

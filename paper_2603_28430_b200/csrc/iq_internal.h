@@ -1,0 +1,66 @@
+// Internal declarations shared by the host parameter builder, the C ABI and
+// the kernel launchers.  Not installed; the public ABI is include/isoquant.h.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "isoquant.h"
+
+namespace iq {
+
+constexpr int kMaxBits = 4;
+constexpr int kMaxHalf = 1 << (kMaxBits - 1);  // h = L/2 <= 8
+
+// Codebook as the kernels see it (passed by value as a kernel parameter, so
+// it lives in the constant bank and is read through uniform registers).
+// Symmetric [R2]: C_{h+m} = cpos[m], C_{h-1-m} = -cpos[m]; thresholds
+// t_{h-1} = 0, t_{h-1+m} = tau[m] = -t_{h-1-m} for m = 1..h-1.
+struct KCodebook {
+  float cpos[kMaxHalf];        // positive centroids, ascending
+  float tau[kMaxHalf];         // tau[0] = 0, tau[m] m>=1 positive thresholds
+  uint32_t tau_bits[kMaxHalf]; // bit patterns of tau (non-negative floats)
+  float cent[2 * kMaxHalf];    // all L centroids ascending (decode lookup)
+};
+
+// Host-side parameter construction (params.cpp): the reference generator of
+// DESIGN.md [R12] and the Lloyd-Max codebook [R1][R2].
+struct HostParams {
+  int d = 0, bits = 0, variant = 0;
+  uint64_t seed = 0;
+  std::vector<double> rot;        // canonical fp64 (see iq_export_params)
+  std::vector<float> mat;         // device operator, fp32 (see iq_export_block_matrices)
+  std::vector<float> centroids;   // [L] fp32 ascending
+  std::vector<float> thresholds;  // [L-1] fp32 ascending
+  KCodebook kcb{};
+};
+
+// Returns false with a message on invalid input.
+bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* hp,
+                       std::string* err);
+size_t rotation_param_count(int d, int variant);
+size_t block_matrix_count(int d, int variant);
+
+// Kernel launchers (kernels.cu).  Each returns a cudaError_t as int.
+struct LaunchArgs {
+  const float* mat;   // device operator
+  KCodebook cb;
+  int64_t n;
+  const void* x;
+  void* y;
+  uint8_t* codes;
+  float* norms;
+  const uint8_t* codes_in;
+  const float* norms_in;
+  double* sums;
+  void* stream;
+};
+
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3 };
+
+// Dispatch to the template instance for (kernel, variant, dtype, d, bits).
+// Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.
+int launch(Kernel k, int variant, int dtype, int d, int bits, const LaunchArgs& a);
+bool gpu_supported(int d, int bits, int variant);
+
+}  // namespace iq

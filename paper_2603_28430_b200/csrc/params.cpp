@@ -1,0 +1,212 @@
+// Host-side parameter construction for IsoQuant stage 1 (runs once per
+// configuration, off the hot path).
+//
+//  * Random fixed block rotations: each unit quaternion is
+//    a normalised N(0, I_4) draw ("Gaussian-normalize sampling on S^3",
+//    P:227); planar angles theta ~ U[0, 2pi) ("uniform angle sampling",
+//    P:227).  Generator: counter-based SplitMix64 -> 53-bit uniforms ->
+//    Box-Muller, reading [R12].
+//  * The per-block operator M = L(q_L) R(conj q_R) (Full) or L(q_L) (Fast),
+//    formed column by column as T(e_j) with Hamilton products in fp64 and
+//    rounded once to fp32; the inverse map conj(q_L) v q_R is exactly M^T
+//    (P:108-110), so the kernels apply M and M^T.
+//  * Scalar codebook: Lloyd-Max for N(0,1) ("per-coordinate Lloyd-Max";
+//    fit unspecified, reading [R1]), exactly symmetrised [R2], scaled by
+//    1/sqrt(d), rounded to fp32; thresholds are fp32 midpoints of adjacent
+//    fp32 centroids [R14b].
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "iq_internal.h"
+
+namespace iq {
+namespace {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kThetaStreamKey = 0x2D358DCCAA6C78A5ull;
+constexpr uint64_t kResampleStride = 1ull << 40;
+
+// k-th output of SplitMix64 seeded with s: mix(s + (k+1) * gamma).
+inline uint64_t splitmix64_at(uint64_t s, uint64_t k) {
+  uint64_t z = s + (k + 1) * kGamma;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Uniform in (0, 1].
+inline double unit_open0(uint64_t s, uint64_t k) {
+  return static_cast<double>((splitmix64_at(s, k) >> 11) + 1) * (1.0 / 9007199254740992.0);
+}
+
+// j-th standard normal: Box-Muller on uniforms (2p, 2p+1), p = j/2;
+// even j -> cosine branch, odd j -> sine branch.
+inline double normal_at(uint64_t s, uint64_t j) {
+  const uint64_t p = j / 2;
+  const double u1 = unit_open0(s, 2 * p);
+  const double u2 = unit_open0(s, 2 * p + 1);
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  const double t = 2.0 * M_PI * u2;
+  return r * ((j % 2 == 0) ? std::cos(t) : std::sin(t));
+}
+
+void unit_quaternion(uint64_t s, uint64_t j0, double q[4]) {
+  for (uint64_t attempt = 0;; ++attempt) {
+    const uint64_t off = j0 + attempt * kResampleStride;
+    double u[4];
+    for (int c = 0; c < 4; ++c) u[c] = normal_at(s, off + c);
+    const double nrm = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2] + u[3] * u[3]);
+    if (nrm >= 1e-12) {
+      for (int c = 0; c < 4; ++c) q[c] = u[c] / nrm;
+      return;
+    }
+  }
+}
+
+// Hamilton product r = a * b, components (w, x, y, z) = w + x i + y j + z k.
+inline void hamilton(const double a[4], const double b[4], double r[4]) {
+  r[0] = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+  r[1] = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+  r[2] = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+  r[3] = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+}
+
+inline double Phi(double x) {
+  if (std::isinf(x)) return x > 0 ? 1.0 : 0.0;
+  return 0.5 * std::erfc(-x / std::sqrt(2.0));
+}
+inline double phi(double x) {
+  if (std::isinf(x)) return 0.0;
+  return std::exp(-0.5 * x * x) / std::sqrt(2.0 * M_PI);
+}
+
+// Inverse normal CDF for the Lloyd start point only (any monotone start
+// converges to the same fixed point): bisection on Phi, fp64.
+double inv_Phi(double p) {
+  double lo = -40.0, hi = 40.0;
+  for (int i = 0; i < 200; ++i) {
+    const double mid = 0.5 * (lo + hi);
+    if (Phi(mid) < p) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// Lloyd-Max levels of a b-bit quantizer for N(0,1), symmetrised exactly.
+std::vector<double> lloyd_max_gaussian(int bits) {
+  const int L = 1 << bits;
+  std::vector<double> c(L), t(L + 1), nc(L);
+  for (int k = 0; k < L; ++k) c[k] = inv_Phi((k + 0.5) / L);
+  const double inf = std::numeric_limits<double>::infinity();
+  for (int it = 0; it < 200000; ++it) {
+    t[0] = -inf;
+    t[L] = inf;
+    for (int k = 0; k + 1 < L; ++k) t[k + 1] = 0.5 * (c[k] + c[k + 1]);
+    double delta = 0.0;
+    for (int k = 0; k < L; ++k) {
+      nc[k] = (phi(t[k]) - phi(t[k + 1])) / (Phi(t[k + 1]) - Phi(t[k]));
+      delta = std::fmax(delta, std::fabs(nc[k] - c[k]));
+    }
+    c.swap(nc);
+    if (delta < 1e-15) break;
+  }
+  const int h = L / 2;
+  std::vector<double> pos(h), out(L);
+  for (int m = 0; m < h; ++m) pos[m] = 0.5 * (c[h + m] - c[h - 1 - m]);
+  for (int m = 0; m < h; ++m) {
+    out[h + m] = pos[m];
+    out[h - 1 - m] = -pos[m];
+  }
+  return out;
+}
+
+}  // namespace
+
+size_t rotation_param_count(int d, int variant) {
+  const size_t g4 = (d + 3) / 4, g2 = (d + 1) / 2;
+  switch (variant) {
+    case IQ_VARIANT_FULL: return 8 * g4;
+    case IQ_VARIANT_FAST: return 4 * g4;
+    case IQ_VARIANT_PLANAR2D: return 2 * g2;
+    default: return 0;
+  }
+}
+
+size_t block_matrix_count(int d, int variant) {
+  if (variant == IQ_VARIANT_PLANAR2D) return 4 * static_cast<size_t>((d + 1) / 2);
+  return 16 * static_cast<size_t>((d + 3) / 4);
+}
+
+bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* hp,
+                       std::string* err) {
+  if (d < 1 || d > (1 << 20)) { *err = "d must be in [1, 2^20]"; return false; }
+  if (bits < 1 || bits > kMaxBits) { *err = "bits must be in [1, 4]"; return false; }
+  if (variant < IQ_VARIANT_FULL || variant > IQ_VARIANT_PLANAR2D) {
+    *err = "variant must be 0 (full), 1 (fast) or 2 (planar2d)";
+    return false;
+  }
+  hp->d = d;
+  hp->bits = bits;
+  hp->variant = variant;
+  hp->seed = seed;
+  hp->rot.assign(rotation_param_count(d, variant), 0.0);
+  hp->mat.assign(block_matrix_count(d, variant), 0.0f);
+
+  if (variant == IQ_VARIANT_PLANAR2D) {
+    const uint64_t s2 = seed ^ kThetaStreamKey;
+    const int g2 = (d + 1) / 2;
+    for (int j = 0; j < g2; ++j) {
+      const double th = 2.0 * M_PI * unit_open0(s2, j);
+      const double c = std::cos(th), s = std::sin(th);
+      hp->rot[2 * j] = c;
+      hp->rot[2 * j + 1] = s;
+      // R(theta) = [[c, -s], [s, c]] row-major
+      float* m = &hp->mat[4 * j];
+      m[0] = static_cast<float>(c);
+      m[1] = static_cast<float>(-s);
+      m[2] = static_cast<float>(s);
+      m[3] = static_cast<float>(c);
+    }
+  } else {
+    const int g = (d + 3) / 4;
+    const bool full = variant == IQ_VARIANT_FULL;
+    for (int b = 0; b < g; ++b) {
+      double qL[4], qR[4] = {1.0, 0.0, 0.0, 0.0};
+      unit_quaternion(seed, 8ull * b, qL);
+      if (full) unit_quaternion(seed, 8ull * b + 4, qR);
+      const int stride = full ? 8 : 4;
+      for (int c = 0; c < 4; ++c) hp->rot[stride * b + c] = qL[c];
+      if (full) for (int c = 0; c < 4; ++c) hp->rot[stride * b + 4 + c] = qR[c];
+      // Column j of M is T(e_j): Full q_L e_j conj(q_R), Fast q_L e_j.
+      const double qRc[4] = {qR[0], -qR[1], -qR[2], -qR[3]};
+      for (int j = 0; j < 4; ++j) {
+        double e[4] = {0, 0, 0, 0}, t1[4], t2[4];
+        e[j] = 1.0;
+        hamilton(qL, e, t1);
+        if (full) hamilton(t1, qRc, t2); else std::memcpy(t2, t1, sizeof t2);
+        for (int i = 0; i < 4; ++i) hp->mat[16 * b + 4 * i + j] = static_cast<float>(t2[i]);
+      }
+    }
+  }
+
+  // Codebook [R1][R2][R14b]
+  const std::vector<double> lv = lloyd_max_gaussian(bits);
+  const int L = 1 << bits, h = L / 2;
+  hp->centroids.resize(L);
+  hp->thresholds.resize(L - 1);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+  for (int k = 0; k < L; ++k) hp->centroids[k] = static_cast<float>(lv[k] * scale);
+  for (int k = 0; k + 1 < L; ++k)
+    hp->thresholds[k] = static_cast<float>(
+        (static_cast<double>(hp->centroids[k]) + static_cast<double>(hp->centroids[k + 1])) * 0.5);
+  KCodebook& kc = hp->kcb;
+  std::memset(&kc, 0, sizeof kc);
+  for (int m = 0; m < h; ++m) kc.cpos[m] = hp->centroids[h + m];
+  for (int m = 1; m < h; ++m) kc.tau[m] = hp->thresholds[h - 1 + m];
+  for (int m = 0; m < kMaxHalf; ++m) std::memcpy(&kc.tau_bits[m], &kc.tau[m], 4);
+  for (int m = h; m < kMaxHalf; ++m) kc.tau_bits[m] = 0xFFFFFFFFu;  // never reached
+  for (int k = 0; k < L; ++k) kc.cent[k] = hp->centroids[k];
+  return true;
+}
+
+}  // namespace iq
