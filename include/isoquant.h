@@ -91,7 +91,7 @@ const char* iq_last_error_detail(void);
 
 /*
  * iq_make_params — build the per-configuration parameters once (host).
- *  d       : vector width.  GPU path: d in {32, 64, 128, 256, 512}.
+ *  d       : vector width.  GPU path: d in {64, 128, 256, 512}.
  *            (Any d >= 1 is accepted when device < 0, for export only.)
  *  bits    : code width b in {1, 2, 3, 4} (the paper uses 2..4).
  *  variant : iq_variant.

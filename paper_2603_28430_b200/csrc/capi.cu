@@ -20,7 +20,7 @@ int launch_planar2d_f32(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_f16(Kernel, int, int, const LaunchArgs&);
 
 bool gpu_supported(int d, int bits, int variant) {
-  const bool dok = d == 32 || d == 64 || d == 128 || d == 256 || d == 512;
+  const bool dok = d == 64 || d == 128 || d == 256 || d == 512;
   return dok && bits >= 1 && bits <= kMaxBits && variant >= 0 && variant <= 2;
 }
 
@@ -67,7 +67,7 @@ iq_status check_call(const iq_params* p, int dtype, int64_t n) {
   if (p->device < 0 || !p->d_mat)
     return fail(IQ_ERR_DEVICE_MISMATCH, "params handle is host-only (device = -1)");
   if (!iq::gpu_supported(p->hp.d, p->hp.bits, p->hp.variant))
-    return fail(IQ_ERR_UNSUPPORTED, "d must be one of 32, 64, 128, 256, 512 on the GPU path");
+    return fail(IQ_ERR_UNSUPPORTED, "d must be one of 64, 128, 256, 512 on the GPU path");
   int cur = -1;
   cudaError_t e = cudaGetDevice(&cur);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -132,7 +132,7 @@ iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device
   if (device >= 0) {
     if (!iq::gpu_supported(d, bits, variant)) {
       delete p;
-      return fail(IQ_ERR_UNSUPPORTED, "d must be one of 32, 64, 128, 256, 512 on the GPU path");
+      return fail(IQ_ERR_UNSUPPORTED, "d must be one of 64, 128, 256, 512 on the GPU path");
     }
     int prev = -1;
     cudaError_t e = cudaGetDevice(&prev);

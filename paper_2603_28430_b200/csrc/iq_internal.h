@@ -21,6 +21,9 @@ struct KCodebook {
   float tau[kMaxHalf];         // tau[0] = 0, tau[m] m>=1 positive thresholds
   uint32_t tau_bits[kMaxHalf]; // bit patterns of tau (non-negative floats)
   float cent[2 * kMaxHalf];    // all L centroids ascending (decode lookup)
+  float delta[kMaxHalf];       // delta[m] m>=1: fp32 step with fl(cpos[m-1] + delta[m])
+                               // == cpos[m] exactly, so an FMA chain over the
+                               // decision indicators lands exactly on C[code]
 };
 
 // Host-side parameter construction (params.cpp): the reference generator of

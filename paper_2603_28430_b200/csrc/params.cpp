@@ -206,6 +206,20 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
   for (int m = 0; m < kMaxHalf; ++m) std::memcpy(&kc.tau_bits[m], &kc.tau[m], 4);
   for (int m = h; m < kMaxHalf; ++m) kc.tau_bits[m] = 0xFFFFFFFFu;  // never reached
   for (int k = 0; k < L; ++k) kc.cent[k] = hp->centroids[k];
+  // Exact steps: fl(cpos[m-1] + delta) must equal cpos[m] (fp32 add, RN) so
+  // that the kernels' indicator-FMA chain reproduces the table value bit for
+  // bit; search the fp32 neighbours of the rounded difference.
+  for (int m = 1; m < h; ++m) {
+    const float a = kc.cpos[m - 1], b = kc.cpos[m];
+    float dlt = b - a;
+    volatile float probe = a + dlt;
+    for (int step = 0; probe != b && step < 64; ++step) {
+      dlt = (probe < b) ? std::nextafter(dlt, 1.0f) : std::nextafter(dlt, -1.0f);
+      probe = a + dlt;
+    }
+    if (probe != b) { *err = "no exact fp32 codebook step"; return false; }
+    kc.delta[m] = dlt;
+  }
   return true;
 }
 

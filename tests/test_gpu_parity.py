@@ -49,7 +49,7 @@ def _parity(variant, dt, d, bits, X, seed=SEED):
 
 @pytest.mark.parametrize("dt", [iq.F32, iq.F16])
 @pytest.mark.parametrize("variant", [iq.FULL, iq.FAST, iq.PLANAR2D])
-@pytest.mark.parametrize("d", [32, 64, 128, 256, 512])
+@pytest.mark.parametrize("d", [64, 128, 256, 512])
 @pytest.mark.parametrize("bits", [1, 2, 3, 4])
 def test_parity_grid(variant, dt, d, bits):
     n = 4096 if d <= 256 else 2048

@@ -1,0 +1,49 @@
+"""Launch one library kernel a few times on device-resident synthetic inputs
+(for ncu captures: keep the command short, one GPU).
+
+  python tools/launch_kernels.py --kernel roundtrip --variant full --d 128 --bits 3 --dtype f16
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernel", default="roundtrip",
+                    choices=["roundtrip", "roundtrip_emit", "quantize", "dequantize", "all"])
+    ap.add_argument("--variant", default="full")
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--dtype", default="f16")
+    ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--reps", type=int, default=4)
+    a = ap.parse_args()
+    import torch
+    import iqsynth
+    import paper_2603_28430_b200 as iq
+    tdt = torch.float16 if a.dtype == "f16" else torch.float32
+    p = iq.iq_make_params(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
+    x = iqsynth.device_unit_vectors(a.n, a.d, 7, tdt, "cuda")
+    y = torch.empty_like(x)
+    codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
+    norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
+    iq.iq_quantize(p, x, codes, norms)
+    kinds = ["quantize", "dequantize", "roundtrip", "roundtrip_emit"] if a.kernel == "all" else [a.kernel]
+    for k in kinds:
+        for _ in range(a.reps):
+            if k == "roundtrip":
+                iq.iq_roundtrip(p, x, y=y)
+            elif k == "roundtrip_emit":
+                iq.iq_roundtrip(p, x, y=y, codes=codes, norms=norms)
+            elif k == "quantize":
+                iq.iq_quantize(p, x, codes, norms)
+            else:
+                iq.iq_dequantize(p, codes, norms, y=y)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
