@@ -28,7 +28,9 @@
  *  - Pointers named x, y, codes, norms, sums are DEVICE pointers on the
  *    params' device, which must be the calling thread's current CUDA device
  *    (else IQ_ERR_DEVICE_MISMATCH).  x and y must be 16-byte aligned, codes
- *    and norms 4-byte aligned (else IQ_ERR_MISALIGNED).  The caller owns all
+ *    and norms 4-byte aligned for iq_quantize / iq_roundtrip and 16-byte
+ *    aligned for iq_dequantize, whose kernel reads them with TMA bulk copies
+ *    (else IQ_ERR_MISALIGNED).  The caller owns all
  *    tensors; the library keeps no reference after the call returns.
  *  - cuda_stream is a cudaStream_t passed as void* (NULL = legacy default).
  *  - Thread-safety: an iq_params handle is immutable after creation and may

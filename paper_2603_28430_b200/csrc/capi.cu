@@ -234,9 +234,8 @@ iq_status iq_dequantize(const iq_params* p, int dtype, int64_t n, const uint8_t*
   if (s != IQ_OK) return s;
   if (n == 0) return IQ_OK;
   if (!y || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms and y are required");
-  if (!aligned(y, 16)) return fail(IQ_ERR_MISALIGNED, "y must be 16-byte aligned");
-  if (!aligned(codes, 4) || !aligned(norms, 4))
-    return fail(IQ_ERR_MISALIGNED, "codes and norms must be 4-byte aligned");
+  if (!aligned(y, 16) || !aligned(codes, 16) || !aligned(norms, 16))
+    return fail(IQ_ERR_MISALIGNED, "y, codes and norms must be 16-byte aligned (TMA bulk loads)");
   iq::LaunchArgs a = base_args(p, n, stream);
   a.codes_in = codes;
   a.norms_in = norms;

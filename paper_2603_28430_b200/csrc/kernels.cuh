@@ -3,24 +3,26 @@
 // and no reuse: it is bound by HBM bandwidth and, at fp16, close to the
 // instruction-issue ceiling.  No tensor cores.  See DESIGN.md "Kernels".
 //
-// Encoder kernels (quantize K1, fused roundtrip K3) are persistent and
-// warp-specialised: one producer warp streams tiles of TILE_V contiguous rows
-// of x from HBM into a ring of shared-memory stages with 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx), so the bytes in flight do not cost
-// registers; NWC compute warps read their rows from shared memory, release
-// the stage, compute in registers and store results with 128-bit streaming
-// stores.  The decoder (K2) reads only d*b/8 + 4 bytes per row and is bound
-// by its stores; it loads codes directly.
+// All three kernels (quantize K1, dequantize K2, fused roundtrip K3) are
+// persistent and warp-specialised.  One producer warp streams tiles of
+// TILE_V contiguous rows from HBM into a ring of shared-memory stages with
+// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx) — rows of x for
+// K1/K3, rows of packed codes plus norms for K2 — so the bytes in flight do
+// not cost registers.  NWC compute warps read their rows from shared memory,
+// release the stage, compute in registers and write results with 128-bit
+// streaming stores.
 //
 // Thread mapping inside a compute warp: a row of d elements of dtype T is cut
-// into 16-byte chunks (EPC = 4 fp32 / 8 fp16 elements); G consecutive lanes
-// serve one row, lane `sub` owning chunks sub, sub+G, ... (CPL chunks), so
-// every warp-wide access of a chunk index is contiguous.  Each lane owns an
-// even number of blocks; blocks are processed two at a time with packed
-// fp32x2 FMAs (FFMA2): the pair (block A, block B) shares every instruction
-// of the rotation.  A lane's blocks never change, so their 4x4 (2x2)
-// operators stay in registers for the whole kernel ("the entire
-// block can often remain in registers from input load through output store").
+// into 16-byte chunks (EPC = 4 fp32 / 8 fp16 elements); G = min(32, d/EPC)
+// consecutive lanes serve one row, lane `sub` owning chunks sub, sub+G, ...
+// (CPL chunks), so every warp-wide access of a chunk index is contiguous.
+// Each lane processes TWO rows at a time: coordinate e of row u0 and of row
+// u1 form one packed fp32x2 register, and every step of the path — norm,
+// rotation, quantizer, inverse rotation, rescale — is one FFMA2/FMUL2/FSET
+// per pair, with the block operator as a broadcast scalar operand.  A lane's
+// blocks never change, so their 4x4 (2x2) operators stay in registers for
+// the whole kernel ("the entire block can often remain in
+// registers from input load through output store").
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -31,38 +33,49 @@
 namespace iq {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNWC = 8;                 // compute warps per encoder CTA
-constexpr int kEncThreads = 32 * (kNWC + 1);
-constexpr int kStageBytes = 16384;      // one TMA stage
-constexpr int kStages = 6;              // ring depth per CTA
-constexpr int kEncSmem = kStages * kStageBytes + 2 * kStages * 8 + 64;
-constexpr int kThreads = 256;           // decoder / statistics CTAs
+constexpr int kNWC = 8;                        // compute warps per CTA
+constexpr int kCtaThreads = 32 * (kNWC + 1);   // + 1 producer warp
+constexpr int kRingBytes = 96 * 1024;          // TMA ring per CTA (2 CTAs / SM)
+constexpr int kThreads = 256;                  // statistics kernel CTAs
 
 template <class T> struct DT;
 template <> struct DT<float> { static constexpr int EPC = 4; };
 template <> struct DT<__half> { static constexpr int EPC = 8; };
 
-template <class T, int D, int VAR>
+template <class T, int D, int BITS, int VAR>
 struct Geo {
   static constexpr int EPC = DT<T>::EPC;
   static constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;   // block width
   static constexpr int CHUNKS = D / EPC;
-  // each lane needs >= 2*PW coordinates so that blocks pair up for FFMA2
-  static constexpr int CPL_MIN = (2 * PW + EPC - 1) / EPC;
-  static constexpr int G = (CHUNKS / CPL_MIN) < 32 ? (CHUNKS / CPL_MIN) : 32;
-  static constexpr int CPL = CHUNKS / G;
-  static constexpr int VPW = 32 / G;
-  static constexpr int EPL = CPL * EPC;          // coordinates per lane
-  static constexpr int NPAIR = EPL / (2 * PW);   // block pairs per lane
-  static constexpr int ROWB = D * (int)sizeof(T);
-  static constexpr int TILE_V = kStageBytes / ROWB;        // rows per TMA stage
-  static constexpr int U = TILE_V / (kNWC * VPW);          // rows per lane group per stage
+  static constexpr int G = CHUNKS < 32 ? CHUNKS : 32;              // lanes per row
+  static constexpr int CPL = CHUNKS / G;                           // chunks per lane
+  static constexpr int VPW = 32 / G;                               // rows per warp
+  static constexpr int EPL = CPL * EPC;                            // coordinates per lane
+  static constexpr int NBL = EPL / PW;                             // blocks per lane
+  static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
+  static constexpr int RB = D * BITS / 8;                          // code bytes per row
+  static constexpr int B = EPC * BITS;                             // code bits per chunk
+  static constexpr int W = G * B / 32;                             // code words per segment
+  // rows per stage: >= 16 KB of x and a whole number of row pairs per warp
+  static constexpr int TV0 = 16384 / ROWB;
+  static constexpr int TILE_V = TV0 > 2 * kNWC * VPW ? TV0 : 2 * kNWC * VPW;
+  static constexpr int U = TILE_V / (kNWC * VPW);                  // rows per lane group per stage
+  static constexpr int ENC_STAGE = TILE_V * ROWB;
+  static constexpr int ENC_STAGES = (kRingBytes / ENC_STAGE) < 8 ? (kRingBytes / ENC_STAGE) : 8;
+  // decoder stage: codes tile (16-B aligned) followed by the norms tile
+  static constexpr int DEC_CODES = (TILE_V * RB + 15) / 16 * 16;
+  static constexpr int DEC_STAGE = DEC_CODES + TILE_V * 4;
+  static constexpr int DEC_STAGES = (kRingBytes / DEC_STAGE) < 8 ? (kRingBytes / DEC_STAGE) : 8;
   static_assert(D % EPC == 0 && (G & (G - 1)) == 0 && CHUNKS % G == 0, "unsupported d");
-  static_assert(EPL % (2 * PW) == 0, "lane must own whole block pairs");
-  static_assert(U >= 1 && TILE_V % (kNWC * VPW) == 0, "stage too small for the warp layout");
-  // decoder: rows per lane group per iteration (16-B stores in flight)
-  static constexpr int UD = (4 / CPL) > 0 ? (4 / CPL) : 1;
+  static_assert(EPL % PW == 0, "lane must own whole blocks");
+  static_assert(U % 2 == 0 && TILE_V % (2 * kNWC * VPW) == 0, "rows pair up");
+  static_assert((G * B) % 32 == 0, "code segment must be whole words");
+  static_assert(ENC_STAGES >= 2 && DEC_STAGES >= 2, "ring too shallow");
 };
+
+// Shared-memory footprint: ring + full/empty barriers + the centroid table.
+template <int STAGE, int NST>
+constexpr int smem_bytes() { return NST * STAGE + 2 * NST * 8 + 64; }
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -81,23 +94,33 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// consumer wait: spin on try_wait (it suspends in hardware between polls)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+// producer wait: back off so a full ring does not steal issue slots from
+// the compute warps sharing its sub-partition
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(256);
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
@@ -113,82 +136,102 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "r"(smem_u32(p)));
   return r;
 }
+__device__ __forceinline__ uint32_t lds32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ float ldsf(const void* p) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(smem_u32(p)));
+  return r;
+}
 __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
   __stcs(reinterpret_cast<uint4*>(p), v);
 }
-__device__ __forceinline__ float sqrt_approx(float x) {
+// MUFU square root / reciprocal square root, flush-to-zero (no denormal
+// fix-up code): the norm of a row with ||x||^2 < 2^-126 is flushed.
+__device__ __forceinline__ float sqrt_ftz(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float rsqrt_approx(float x) {
+__device__ __forceinline__ float rsqrt_ftz(float x) {
   float r;
-  asm("rsqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
-}
-
-// ----------------------------------------------------------- dtype <-> fp32
-template <class T> __device__ __forceinline__ void to_f32(const uint4& r, float* f);
-template <> __device__ __forceinline__ void to_f32<float>(const uint4& r, float* f) {
-  f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
-  f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
-}
-template <> __device__ __forceinline__ void to_f32<__half>(const uint4& r, float* f) {
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-    f[2 * k] = t.x; f[2 * k + 1] = t.y;
-  }
-}
-template <class T> __device__ __forceinline__ uint4 from_f32(const float* f);
-template <> __device__ __forceinline__ uint4 from_f32<float>(const float* f) {
-  return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
-                    __float_as_uint(f[3]));
-}
-template <> __device__ __forceinline__ uint4 from_f32<__half>(const float* f) {
-  uint32_t w[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    __half2 h = __floats2half2_rn(f[2 * k], f[2 * k + 1]);  // round-to-nearest-even [R15]
-    w[k] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // ------------------------------------------------------------ packed fp32x2
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
-// Lane coordinate of element j of block A / B in block pair k (lane-local
-// coordinates are chunk-major: coordinate c*EPC + e is element e of the
-// lane's chunk c).
-template <int PW> __device__ __forceinline__ constexpr int coordA(int k, int j) { return 2 * PW * k + j; }
-template <int PW> __device__ __forceinline__ constexpr int coordB(int k, int j) { return 2 * PW * k + PW + j; }
+// chunk (16 B) of two rows -> EPC coordinate pairs (row u0 in .x, u1 in .y)
+template <class T> __device__ __forceinline__ void to_pairs(const uint4& a, const uint4& b, float2* p);
+template <> __device__ __forceinline__ void to_pairs<float>(const uint4& a, const uint4& b, float2* p) {
+  p[0] = f2(__uint_as_float(a.x), __uint_as_float(b.x));
+  p[1] = f2(__uint_as_float(a.y), __uint_as_float(b.y));
+  p[2] = f2(__uint_as_float(a.z), __uint_as_float(b.z));
+  p[3] = f2(__uint_as_float(a.w), __uint_as_float(b.w));
+}
+template <> __device__ __forceinline__ void to_pairs<__half>(const uint4& a, const uint4& b, float2* p) {
+  const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 ta = __half22float2(*reinterpret_cast<const __half2*>(&wa[k]));
+    const float2 tb = __half22float2(*reinterpret_cast<const __half2*>(&wb[k]));
+    p[2 * k] = f2(ta.x, tb.x);
+    p[2 * k + 1] = f2(ta.y, tb.y);
+  }
+}
+// EPC coordinate pairs -> the two rows' 16-byte chunks (fp16: RN-even [R15])
+template <class T> __device__ __forceinline__ void from_pairs(const float2* p, uint4& a, uint4& b);
+template <> __device__ __forceinline__ void from_pairs<float>(const float2* p, uint4& a, uint4& b) {
+  a = make_uint4(__float_as_uint(p[0].x), __float_as_uint(p[1].x), __float_as_uint(p[2].x),
+                 __float_as_uint(p[3].x));
+  b = make_uint4(__float_as_uint(p[0].y), __float_as_uint(p[1].y), __float_as_uint(p[2].y),
+                 __float_as_uint(p[3].y));
+}
+template <> __device__ __forceinline__ void from_pairs<__half>(const float2* p, uint4& a, uint4& b) {
+  uint32_t wa[4], wb[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __half2 ha = __floats2half2_rn(p[2 * k].x, p[2 * k + 1].x);
+    __half2 hb = __floats2half2_rn(p[2 * k].y, p[2 * k + 1].y);
+    wa[k] = *reinterpret_cast<uint32_t*>(&ha);
+    wb[k] = *reinterpret_cast<uint32_t*>(&hb);
+  }
+  a = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+  b = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+}
 
-// Paired block operator: M2[i*PW+j] = (M_A[i][j], M_B[i][j]).
-// forward y = M x (+0-started dot products: a rotated coordinate is never -0,
-// so the sign test below classifies +-0 exactly like the count definition).
+// ----------------------------------------------------------- block operator
+// M (row-major PW x PW): forward y = M v, inverse v = M^T c.  4-D: M =
+// L(q_L) R(conj q_R) (Full) / L(q_L) (Fast); the inverse sandwich conj(q_L)
+// v q_R is exactly M^T (Proposition).  2-D: M = R(theta) and
+// R(-theta) = R(theta)^T.  Forward dot products start from +0, so a
+// rotated coordinate is never -0 and the sign test of the quantizer
+// classifies +-0 exactly like the count definition (both go up) [R3].
 template <int PW>
-__device__ __forceinline__ void rot_fwd2(const float2* M2, const float2* x, float2* y) {
+__device__ __forceinline__ void rot_fwd(const float* M, const float2* x, float2* y) {
 #pragma unroll
   for (int i = 0; i < PW; ++i) {
-    float2 a = fma2(M2[PW * i], x[0], f2(0.0f, 0.0f));
+    float2 a = fma2(x[0], bc(M[PW * i]), bc(0.0f));
 #pragma unroll
-    for (int j = 1; j < PW; ++j) a = fma2(M2[PW * i + j], x[j], a);
+    for (int j = 1; j < PW; ++j) a = fma2(x[j], bc(M[PW * i + j]), a);
     y[i] = a;
   }
 }
-// inverse v = M^T c: the inverse sandwich conj(q_L) v q_R is exactly M^T
-// (Proposition); R(-theta) = R(theta)^T.
 template <int PW>
-__device__ __forceinline__ void rot_inv2(const float2* M2, const float2* c, float2* v) {
+__device__ __forceinline__ void rot_inv(const float* M, const float2* c, float2* v) {
 #pragma unroll
   for (int j = 0; j < PW; ++j) {
-    float2 a = mul2(M2[j], c[0]);
+    float2 a = mul2(c[0], bc(M[j]));
 #pragma unroll
-    for (int i = 1; i < PW; ++i) a = fma2(M2[PW * i + j], c[i], a);
+    for (int i = 1; i < PW; ++i) a = fma2(c[i], bc(M[PW * i + j]), a);
     v[j] = a;
   }
 }
@@ -198,45 +241,45 @@ __device__ __forceinline__ void rot_inv2(const float2* M2, const float2* c, floa
 // out-of-range clamps) [R3][R4]:
 //   y >= 0 : code = h + m,          m = #{i >= 1 : y >= tau_i}
 //   y <  0 : code = h - 1 - m,      m = #{i >= 1 : |y| > tau_i}
-// For positive floats |y| > tau <=> nextdown(|y|) >= tau, and nextdown is
-// "bits - 1", so key = bits(|y|) - s (s = sign bit) turns both cases into
-// key >= tau (compared as floats; key is a non-negative float).  With H = h,
-// h - 1 - m = m ^ (h - 1) and h + m = m ^ h, so code = m ^ (h - s).
-// Decision in fp32, the kernel's precision [R14b].
-__device__ __forceinline__ uint32_t sign_of(float y) { return __float_as_uint(y) >> 31; }
-__device__ __forceinline__ float key_of(float y) {
-  const uint32_t b = __float_as_uint(y);
-  return __uint_as_float(b - (b >> 31) * 0x80000001u);
+// For positive floats |y| > tau <=> nextdown(|y|) >= tau and nextdown is
+// "bits - 1", so key = bits(y) + s * 0x7fffffff (s = sign bit; = bits(|y|) - s
+// mod 2^32) turns both cases into key >= tau, compared as floats.  With
+// m < h: h + m = m ^ h and h - 1 - m = m ^ (h - 1), so code = m ^ (h - s).
+// The decision is taken in fp32, the kernel's precision [R14b].
+__device__ __forceinline__ uint32_t sbit(float y) { return __float_as_uint(y) >> 31; }
+__device__ __forceinline__ float key_of(float y, uint32_t s) {
+  uint32_t k;
+  asm("mad.lo.u32 %0, %1, 2147483647, %2;" : "=r"(k) : "r"(s), "r"(__float_as_uint(y)));
+  return __uint_as_float(k);
+}
+__device__ __forceinline__ float sign_xor(float c, float y) {
+  return __uint_as_float(__float_as_uint(c) ^ (__float_as_uint(y) & 0x80000000u));
 }
 
-// Signed centroid values of a coordinate pair (roundtrip without codes):
-// c = cpos[0] + sum_i [key >= tau_i] * (cpos[i] - cpos[i-1]), sign of y.
-template <int BITS>
-__device__ __forceinline__ float2 qvalue2(float2 y, const KCodebook& cb) {
+// One coordinate pair through Q.  Returns the signed centroids (both rows);
+// with CODES also the two codes.  The centroid is accumulated as
+// cpos[0] + sum_i [key >= tau_i] * delta_i with fp32 steps chosen on the host
+// so that the chain lands exactly on C[code] (see params.cpp).
+template <int BITS, bool CODES>
+__device__ __forceinline__ float2 quantize_pair(float2 y, const KCodebook& cb, uint32_t& code_a,
+                                                uint32_t& code_b) {
   constexpr int H = 1 << (BITS - 1);
-  const float ka = key_of(y.x), kb = key_of(y.y);
-  float2 c = f2(cb.cpos[0], cb.cpos[0]);
+  const uint32_t sa = sbit(y.x), sb = sbit(y.y);
+  const float ka = key_of(y.x, sa), kb = key_of(y.y, sb);
+  float2 c = bc(cb.cpos[0]);
+  float2 m = bc(8388608.0f);  // 2^23: the count lands in the low mantissa bits
 #pragma unroll
   for (int i = 1; i < H; ++i) {
     const float2 g = f2(ka >= cb.tau[i] ? 1.0f : 0.0f, kb >= cb.tau[i] ? 1.0f : 0.0f);
-    c = fma2(g, f2(cb.delta[i], cb.delta[i]), c);
+    c = fma2(g, bc(cb.delta[i]), c);
+    if (CODES) m = add2(m, g);
   }
-  return f2(__uint_as_float(__float_as_uint(c.x) ^ (__float_as_uint(y.x) & 0x80000000u)),
-            __uint_as_float(__float_as_uint(c.y) ^ (__float_as_uint(y.y) & 0x80000000u)));
+  if (CODES) {
+    code_a = (__float_as_uint(m.x) ^ (uint32_t)(H - (int)sa)) & (2u * H - 1u);
+    code_b = (__float_as_uint(m.y) ^ (uint32_t)(H - (int)sb)) & (2u * H - 1u);
+  }
+  return f2(sign_xor(c.x, y.x), sign_xor(c.y, y.y));
 }
-
-// Code (and, through the shared-memory table s_cpos, the signed centroid).
-template <int BITS>
-__device__ __forceinline__ uint32_t qcode(float y, const KCodebook& cb) {
-  constexpr int H = 1 << (BITS - 1);
-  const float k = key_of(y);
-  uint32_t m = 0;
-#pragma unroll
-  for (int i = 1; i < H; ++i) m += (k >= cb.tau[i]) ? 1u : 0u;
-  return m ^ (uint32_t)(H - (int)sign_of(y));
-}
-// signed centroid from the code: C[code], symmetric table in shared memory
-__device__ __forceinline__ float centroid_of(uint32_t code, const float* s_cent) { return s_cent[code]; }
 
 // ------------------------------------------------------------- bit packing
 // A lane's chunk contributes B = EPC*BITS consecutive bits of the row's
@@ -271,38 +314,35 @@ __device__ __forceinline__ uint32_t gather_word(uint32_t bits, int sub, int vbas
   }
 }
 
-// The B bits of lane `sub` from the segment's words (word t held by lane t).
-template <int G, int B>
-__device__ __forceinline__ uint32_t scatter_bits(uint32_t word, int sub, int vbase) {
-  if constexpr (B == 32) {
-    return word;
-  } else {
-    constexpr int W = G * B / 32;
-    const int off = sub * B;
-    const int w0 = off >> 5, sh = off & 31;
-    const uint32_t lo = __shfl_sync(kFull, word, vbase + w0);
-    const uint32_t hi = __shfl_sync(kFull, word, vbase + (w0 + 1 < W ? w0 + 1 : W - 1));
-    uint32_t r = (sh == 0) ? lo : ((lo >> sh) | (hi << (32 - sh)));
-    return r & ((1u << B) - 1u);
+// Load a lane's block operators: lane coordinate c*EPC + e is global
+// coordinate (sub + c*G)*EPC + e; block b of the lane covers lane coordinates
+// b*PW .. b*PW+PW-1 (blocks never straddle a chunk since PW divides EPC).
+template <class Gm>
+__device__ __forceinline__ void load_ops(const float* __restrict__ mat, int sub,
+                                         float (&P)[Gm::NBL][Gm::PW * Gm::PW]) {
+  constexpr int PW = Gm::PW, EPC = Gm::EPC, G = Gm::G, NPB = PW * PW;
+#pragma unroll
+  for (int b = 0; b < Gm::NBL; ++b) {
+    const int lc = b * PW;
+    const int gc = (sub + (lc / EPC) * G) * EPC + lc % EPC;
+    const float4* m = reinterpret_cast<const float4*>(mat + (size_t)(gc / PW) * NPB);
+#pragma unroll
+    for (int q = 0; q < NPB / 4; ++q) {
+      const float4 t = __ldg(m + q);
+      P[b][4 * q] = t.x; P[b][4 * q + 1] = t.y; P[b][4 * q + 2] = t.z; P[b][4 * q + 3] = t.w;
+    }
   }
 }
 
-// Load a lane's paired operators: pair k = blocks A (lane coords 2PWk..) and
-// B (2PWk+PW..).  Lane coordinate c*EPC+e <-> global coordinate
-// (sub + c*G)*EPC + e, so block index = global coordinate / PW.
-template <class Gm>
-__device__ __forceinline__ void load_ops(const float* __restrict__ mat, int sub,
-                                         float2 (&P)[Gm::NPAIR][Gm::PW * Gm::PW]) {
-  constexpr int PW = Gm::PW, EPC = Gm::EPC, G = Gm::G, NPB = PW * PW;
-#pragma unroll
-  for (int k = 0; k < Gm::NPAIR; ++k) {
-    const int la = coordA<PW>(k, 0), lb = coordB<PW>(k, 0);
-    const int ga = (sub + (la / EPC) * G) * EPC + la % EPC;
-    const int gb = (sub + (lb / EPC) * G) * EPC + lb % EPC;
-    const float* ma = mat + (size_t)(ga / PW) * NPB;
-    const float* mb = mat + (size_t)(gb / PW) * NPB;
-#pragma unroll
-    for (int q = 0; q < NPB; ++q) P[k][q] = f2(__ldg(ma + q), __ldg(mb + q));
+// Ring setup shared by the three kernels.
+template <int NST>
+__device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNWC);
+    }
+    fence_mbar_init();
   }
 }
 
@@ -310,32 +350,22 @@ __device__ __forceinline__ void load_ops(const float* __restrict__ mat, int sub,
 // MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y; codes and
 // norms too when `codes` is non-null).
 template <class T, int D, int BITS, int VAR, int MODE>
-__global__ void __launch_bounds__(kEncThreads)
+__global__ void __launch_bounds__(kCtaThreads)
 k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x, T* y,
          uint8_t* __restrict__ codes, float* __restrict__ norms) {
-  using Gm = Geo<T, D, VAR>;
+  using Gm = Geo<T, D, BITS, VAR>;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
-  constexpr int PW = Gm::PW, NPAIR = Gm::NPAIR, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
-  constexpr int B = EPC * BITS, W = G * B / 32, RB = D * BITS / 8;
-  constexpr int L = 1 << BITS;
-  static_assert((G * B) % 32 == 0, "segment must be whole words");
+  constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
+  constexpr int B = Gm::B, W = Gm::W, RB = Gm::RB;
+  constexpr int STAGE = Gm::ENC_STAGE, NST = Gm::ENC_STAGES;
 
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  float* s_cent = reinterpret_cast<float*>(empty + kStages);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNWC);
-    }
-    fence_mbar_init();
-  }
-  if (threadIdx.x < L) s_cent[threadIdx.x] = cb.cent[threadIdx.x];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+  uint64_t* empty = full + NST;
+  ring_init<NST>(full, empty);
   __syncthreads();
 
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + TILE_V - 1) / TILE_V;
 
   if (warp == kNWC) {  // ---------------- producer: TMA bulk loads into the ring
@@ -344,13 +374,13 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait_backoff(&empty[s], ph ^ 1);
         const int64_t v0 = t * TILE_V;
         const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
         const uint32_t bytes = (uint32_t)(nv * Gm::ROWB);
         mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(smem + s * kStageBytes, x + v0 * D, bytes, &full[s], pol);
-        if (++s == kStages) { s = 0; ph ^= 1; }
+        bulk_g2s(smem + s * STAGE, x + v0 * D, bytes, &full[s], pol);
+        if (++s == NST) { s = 0; ph ^= 1; }
       }
     }
     return;
@@ -360,7 +390,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   const int sub = lane & (G - 1);
   const int vbase = lane & ~(G - 1);
   const int vslot = lane / G;
-  float2 P[NPAIR][PW * PW];
+  float P[NBL][PW * PW];
   load_ops<Gm>(mat, sub, P);
   const bool emit = (MODE == 0) || (codes != nullptr);
 
@@ -368,159 +398,231 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   uint32_t ph = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&full[s], ph);
-    const uint8_t* st = smem + s * kStageBytes;
+    const uint8_t* st = smem + s * STAGE;
     uint4 raw[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int vl = (warp * U + u) * VPW + vslot;   // row within the tile
+      const int vl = (warp * U + u) * VPW + vslot;  // row within the tile
 #pragma unroll
-      for (int i = 0; i < CPL; ++i)
-        raw[u][i] = lds128(st + (size_t)vl * Gm::ROWB + (sub + i * G) * 16);
+      for (int i = 0; i < CPL; ++i) raw[u][i] = lds128(st + vl * Gm::ROWB + (sub + i * G) * 16);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);           // stage may be refilled
-    if (++s == kStages) { s = 0; ph ^= 1; }
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage may be refilled
+    if (++s == NST) { s = 0; ph ^= 1; }
 
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t vec = t * TILE_V + (warp * U + u) * VPW + vslot;
-      const bool valid = vec < n;
-      float v[EPL];
+    for (int u = 0; u < U; u += 2) {  // rows u (.x) and u+1 (.y)
+      const int64_t va = t * TILE_V + (warp * U + u) * VPW + vslot;
+      const int64_t vb = va + VPW;
+      float2 v[EPL];
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) to_f32<T>(raw[u][i], v + i * EPC);
+      for (int i = 0; i < CPL; ++i) to_pairs<T>(raw[u][i], raw[u + 1][i], v + i * EPC);
       // Alg.1 l.1: rho = ||x||, xbar = x / max(rho, eps)  [R5]
-      float2 ss2 = f2(0.0f, 0.0f);
+      float2 ss = mul2(v[0], v[0]);
 #pragma unroll
-      for (int e = 0; e < EPL; e += 2) ss2 = fma2(f2(v[e], v[e + 1]), f2(v[e], v[e + 1]), ss2);
-      float ss = ss2.x + ss2.y;
+      for (int e = 1; e < EPL; ++e) ss = fma2(v[e], v[e], ss);
 #pragma unroll
-      for (int o = G / 2; o >= 1; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
-      const float rho = sqrt_approx(ss);
-      const float inv = rsqrt_approx(fmaxf(ss, 1e-24f));
-      const float2 inv2 = f2(inv, inv), rho2 = f2(rho, rho);
+      for (int o = G / 2; o >= 1; o >>= 1)
+        ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
+      const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
+      const float2 inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));
 
-      float out[EPL];
-      uint32_t cw[CPL];
+      float2 out[EPL];
+      uint32_t cwa[CPL], cwb[CPL];
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) cw[i] = 0;
+      for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
 #pragma unroll
-      for (int k = 0; k < NPAIR; ++k) {
-        float2 xb[PW], yb[PW], cq[PW], rb[PW];
+      for (int b = 0; b < NBL; ++b) {
+        float2 xb[PW], yb[PW], cq[PW];
 #pragma unroll
-        for (int j = 0; j < PW; ++j) xb[j] = mul2(f2(v[coordA<PW>(k, j)], v[coordB<PW>(k, j)]), inv2);
-        rot_fwd2<PW>(P[k], xb, yb);                          // v~ = T(v)   (Alg.1 l.5/9/13)
-        if (emit) {
+        for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);
+        rot_fwd<PW>(P[b], xb, yb);                       // v~ = T(v)     (Alg.1 l.5/9/13)
 #pragma unroll
-          for (int j = 0; j < PW; ++j) {
-            const uint32_t ca = qcode<BITS>(yb[j].x, cb), cbb = qcode<BITS>(yb[j].y, cb);
-            const int la = coordA<PW>(k, j), lb = coordB<PW>(k, j);
-            cw[la / EPC] += ca << ((la % EPC) * BITS);
-            cw[lb / EPC] += cbb << ((lb % EPC) * BITS);
-            if (MODE == 1) cq[j] = f2(centroid_of(ca, s_cent), centroid_of(cbb, s_cent));
+        for (int j = 0; j < PW; ++j) {
+          const int lc = b * PW + j;                     // lane coordinate
+          if (emit) {
+            uint32_t ca, cb2;
+            cq[j] = quantize_pair<BITS, true>(yb[j], cb, ca, cb2);   // v^ = Q(v~)
+            cwa[lc / EPC] |= ca << ((lc % EPC) * BITS);
+            cwb[lc / EPC] |= cb2 << ((lc % EPC) * BITS);
+          } else {
+            uint32_t dummy0, dummy1;
+            cq[j] = quantize_pair<BITS, false>(yb[j], cb, dummy0, dummy1);
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < PW; ++j) cq[j] = qvalue2<BITS>(yb[j], cb);   // v^ = Q(v~)
         }
         if (MODE == 1) {
-          rot_inv2<PW>(P[k], cq, rb);                        // v_rec = T^-1(v^)
+          float2 rb[PW];
+          rot_inv<PW>(P[b], cq, rb);                     // v_rec = T^-1(v^)
 #pragma unroll
-          for (int j = 0; j < PW; ++j) {
-            const float2 o = mul2(rb[j], rho2);              // x^ = rho * v_rec
-            out[coordA<PW>(k, j)] = o.x;
-            out[coordB<PW>(k, j)] = o.y;
-          }
+          for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(rb[j], rho);   // x^ = rho * v_rec
         }
       }
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
-        if (MODE == 1 && valid) st_stream(y + vec * D + (sub + i * G) * EPC, from_f32<T>(out + i * EPC));
+        if (MODE == 1) {
+          uint4 oa, ob;
+          from_pairs<T>(out + i * EPC, oa, ob);
+          const size_t off = (size_t)(sub + i * G) * EPC;
+          if (va < n) st_stream(y + va * D + off, oa);
+          if (vb < n) st_stream(y + vb * D + off, ob);
+        }
         if (emit) {
-          const uint32_t word = gather_word<G, B>(cw[i], sub, vbase);
-          if (valid && sub < W)
-            *reinterpret_cast<uint32_t*>(codes + vec * RB + 4 * (i * W + sub)) = word;
+          const uint32_t wa = gather_word<G, B>(cwa[i], sub, vbase);
+          const uint32_t wb = gather_word<G, B>(cwb[i], sub, vbase);
+          if (sub < W) {
+            if (va < n) *reinterpret_cast<uint32_t*>(codes + va * RB + 4 * (i * W + sub)) = wa;
+            if (vb < n) *reinterpret_cast<uint32_t*>(codes + vb * RB + 4 * (i * W + sub)) = wb;
+          }
         }
       }
-      if (emit && valid && sub == 0) norms[vec] = rho;
+      if (emit && sub == 0) {
+        if (va < n) norms[va] = rho.x;
+        if (vb < n) norms[vb] = rho.y;
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- decoder (K2)
+// Ring stage = TILE_V rows of packed codes (RB bytes each) + their norms.
 template <class T, int D, int BITS, int VAR>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kCtaThreads)
 k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
          const uint8_t* __restrict__ codes, const float* __restrict__ norms, T* __restrict__ y) {
-  using Gm = Geo<T, D, VAR>;
-  constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::UD;
-  constexpr int PW = Gm::PW, NPAIR = Gm::NPAIR, EPL = Gm::EPL;
-  constexpr int B = EPC * BITS, W = G * B / 32, RB = D * BITS / 8;
+  using Gm = Geo<T, D, BITS, VAR>;
+  constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
+  constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
+  constexpr int B = Gm::B, W = Gm::W, RB = Gm::RB;
+  constexpr int STAGE = Gm::DEC_STAGE, NST = Gm::DEC_STAGES, CODES_B = Gm::DEC_CODES;
   constexpr int L = 1 << BITS;
 
-  __shared__ float s_cent[L];
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+  uint64_t* empty = full + NST;
+  float* s_cent = reinterpret_cast<float*>(empty + NST);
+  ring_init<NST>(full, empty);
   if (threadIdx.x < L) s_cent[threadIdx.x] = cb.cent[threadIdx.x];
   __syncthreads();
 
-  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TILE_V - 1) / TILE_V;
+
+  if (warp == kNWC) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait_backoff(&empty[s], ph ^ 1);
+        const int64_t v0 = t * TILE_V;
+        const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
+        const uint32_t cbytes = (uint32_t)(nv * RB), nbytes = (uint32_t)(nv * 4);
+        // bulk copies need 16-byte sizes: round up inside the row arrays only
+        // when the rounded range stays within the caller's buffers (the tail
+        // tile rounds down and the remainder is read directly, see below).
+        const uint32_t c16 = cbytes & ~15u, n16 = nbytes & ~15u;
+        if (c16 + n16 == 0) {
+          mbar_arrive(&full[s]);
+        } else {
+          mbar_arrive_expect_tx(&full[s], c16 + n16);
+          if (c16) bulk_g2s(smem + s * STAGE, codes + v0 * RB, c16, &full[s], pol);
+          if (n16) bulk_g2s(smem + s * STAGE + CODES_B, norms + v0, n16, &full[s], pol);
+        }
+        if (++s == NST) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+
   const int sub = lane & (G - 1);
-  const int vbase = lane & ~(G - 1);
   const int vslot = lane / G;
-  float2 P[NPAIR][PW * PW];
+  float P[NBL][PW * PW];
   load_ops<Gm>(mat, sub, P);
 
-  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-  const int64_t ntiles = (n + VPW * U - 1) / (VPW * U);
-  for (int64_t tile = warp; tile < ntiles; tile += nwarps) {
-    uint32_t wd[U][CPL];
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], ph);
+    const uint8_t* st = smem + s * STAGE;
+    const int64_t v0 = t * TILE_V;
+    const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
+    const int64_t c16 = (nv * RB) & ~(int64_t)15, n16 = (nv * 4) & ~(int64_t)15;
+    uint32_t bits[U][CPL];
     float rho[U];
-    int64_t vec[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      vec[u] = tile * (VPW * U) + u * VPW + vslot;
-      const bool valid = vec[u] < n;
+      const int vl = (warp * U + u) * VPW + vslot;
+      const bool valid = vl < nv;
 #pragma unroll
-      for (int i = 0; i < CPL; ++i)
-        wd[u][i] = (valid && sub < W)
-            ? __ldcs(reinterpret_cast<const unsigned int*>(codes + vec[u] * RB + 4 * (i * W + sub)))
-            : 0u;
-      rho[u] = valid ? __ldcs(norms + vec[u]) : 0.0f;
+      for (int i = 0; i < CPL; ++i) {
+        // this lane's B bits start at bit (i*G + sub)*B of the row
+        const int bit0 = (i * G + sub) * B;
+        const int byte0 = vl * RB + (bit0 >> 5) * 4;
+        const int sh = bit0 & 31;
+        uint32_t lo = 0, hi = 0;
+        if (valid) {
+          lo = (byte0 + 4 <= c16) ? lds32(st + byte0) : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0));
+          if (B < 32 && sh + B > 32)
+            hi = (byte0 + 8 <= c16) ? lds32(st + byte0 + 4)
+                                    : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0 + 4));
+        }
+        uint32_t r = (sh == 0) ? lo : ((lo >> sh) | (hi << (32 - sh)));
+        if (B < 32) r &= (1u << (B & 31)) - 1u;
+        bits[u][i] = r;
+      }
+      rho[u] = valid ? ((vl * 4 + 4 <= n16) ? ldsf(st + CODES_B + vl * 4) : __ldg(norms + v0 + vl)) : 0.0f;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == NST) { s = 0; ph ^= 1; }
+
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint32_t bits[CPL];
+    for (int u = 0; u < U; u += 2) {
+      const int64_t va = v0 + (warp * U + u) * VPW + vslot;
+      const int64_t vb = va + VPW;
+      const float2 r2 = f2(rho[u], rho[u + 1]);
+      float2 out[EPL];
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) bits[i] = scatter_bits<G, B>(wd[u][i], sub, vbase);
-      const float2 rho2 = f2(rho[u], rho[u]);
-      float out[EPL];
-#pragma unroll
-      for (int k = 0; k < NPAIR; ++k) {
+      for (int b = 0; b < NBL; ++b) {
         float2 cq[PW], rb[PW];
 #pragma unroll
         for (int j = 0; j < PW; ++j) {
-          const int la = coordA<PW>(k, j), lb = coordB<PW>(k, j);
-          const uint32_t ca = (bits[la / EPC] >> ((la % EPC) * BITS)) & (L - 1);
-          const uint32_t cbb = (bits[lb / EPC] >> ((lb % EPC) * BITS)) & (L - 1);
-          cq[j] = f2(s_cent[ca], s_cent[cbb]);             // v^ = C[code]
+          const int lc = b * PW + j;
+          const uint32_t ca = (bits[u][lc / EPC] >> ((lc % EPC) * BITS)) & (L - 1);
+          const uint32_t cbb = (bits[u + 1][lc / EPC] >> ((lc % EPC) * BITS)) & (L - 1);
+          cq[j] = f2(s_cent[ca], s_cent[cbb]);            // v^ = C[code]
         }
-        rot_inv2<PW>(P[k], cq, rb);                         // T^-1
+        rot_inv<PW>(P[b], cq, rb);                        // T^-1
 #pragma unroll
-        for (int j = 0; j < PW; ++j) {
-          const float2 o = mul2(rb[j], rho2);               // x^ = rho * ...
-          out[coordA<PW>(k, j)] = o.x;
-          out[coordB<PW>(k, j)] = o.y;
-        }
+        for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(rb[j], r2);   // x^ = rho * ...
       }
-      if (vec[u] < n) {
 #pragma unroll
-        for (int i = 0; i < CPL; ++i)
-          st_stream(y + vec[u] * D + (sub + i * G) * EPC, from_f32<T>(out + i * EPC));
+      for (int i = 0; i < CPL; ++i) {
+        uint4 oa, ob;
+        from_pairs<T>(out + i * EPC, oa, ob);
+        const size_t off = (size_t)(sub + i * G) * EPC;
+        if (va < n) st_stream(y + va * D + off, oa);
+        if (vb < n) st_stream(y + vb * D + off, ob);
       }
     }
   }
 }
 
 // ------------------------------------------------ reconstruction statistics
+template <class T> __device__ __forceinline__ void to_f32(const uint4& r, float* f);
+template <> __device__ __forceinline__ void to_f32<float>(const uint4& r, float* f) {
+  f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
+  f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+}
+template <> __device__ __forceinline__ void to_f32<__half>(const uint4& r, float* f) {
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    f[2 * k] = t.x; f[2 * k + 1] = t.y;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kThreads)
 k_error_sums(int64_t nchunks, const T* __restrict__ x, const T* __restrict__ y, double* sums) {
