@@ -281,13 +281,14 @@ def main():
     for i in range(a.warmup):
         step(i)
     torch.cuda.synchronize()
-    sampler = ClockSampler(local) if (rank == 0 and not a.profile) else None
+    sampler = ClockSampler(local) if (rank == 0 and not a.profile and not os.environ.get("IQ_NO_SAMPLER")) else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
     t_load0 = time.time()
     i = 0
-    while not a.profile and time.time() - t_load0 < 0.4:   # untimed clock settle under load
+    settle = float(os.environ.get("IQ_SETTLE_S", "0.4"))
+    while not a.profile and time.time() - t_load0 < settle:   # untimed clock settle under load
         step(i)
         i += 1
         if i % 64 == 0:

@@ -71,6 +71,9 @@ struct Geo {
   static_assert(U % 2 == 0 && TILE_V % (2 * kNWC * VPW) == 0, "rows pair up");
   static_assert((G * B) % 32 == 0, "code segment must be whole words");
   static_assert(ENC_STAGES >= 2 && DEC_STAGES >= 2, "ring too shallow");
+  // 2 CTAs (16 compute warps) per SM when a lane's operators fit (<= 96
+  // registers per thread with 18 warps per SM); 1 CTA for d=512
+  static constexpr int MIN_CTAS = NBL * PW * PW <= 32 ? 2 : 1;
 };
 
 // Shared-memory footprint: ring + full/empty barriers + the centroid table.
@@ -94,26 +97,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
+// Blocking wait: try_wait with a suspend-time hint parks the thread in
+// hardware until the phase completes (no issue slots burnt while waiting).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
       : "memory");
-  return ok != 0;
-}
-// consumer wait: spin on try_wait (it suspends in hardware between polls)
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) {
-  }
-}
-// producer wait: back off so a full ring does not steal issue slots from
-// the compute warps sharing its sub-partition
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) __nanosleep(256);
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -237,48 +230,95 @@ __device__ __forceinline__ void rot_inv(const float* M, const float2* c, float2*
 }
 
 // --------------------------------------------------------------- quantizer Q
-// code = #{k : y >= t_k} over the symmetric fp32 thresholds (ties go up,
-// out-of-range clamps) [R3][R4]:
-//   y >= 0 : code = h + m,          m = #{i >= 1 : y >= tau_i}
-//   y <  0 : code = h - 1 - m,      m = #{i >= 1 : |y| > tau_i}
-// For positive floats |y| > tau <=> nextdown(|y|) >= tau and nextdown is
-// "bits - 1", so key = bits(y) + s * 0x7fffffff (s = sign bit; = bits(|y|) - s
-// mod 2^32) turns both cases into key >= tau, compared as floats.  With
-// m < h: h + m = m ^ h and h - 1 - m = m ^ (h - 1), so code = m ^ (h - s).
-// The decision is taken in fp32, the kernel's precision [R14b].
-__device__ __forceinline__ uint32_t sbit(float y) { return __float_as_uint(y) >> 31; }
-__device__ __forceinline__ float key_of(float y, uint32_t s) {
-  uint32_t k;
-  asm("mad.lo.u32 %0, %1, 2147483647, %2;" : "=r"(k) : "r"(s), "r"(__float_as_uint(y)));
-  return __uint_as_float(k);
+// code = #{k : ybar >= t_k} over the symmetric fp32 thresholds (ties go up,
+// out-of-range clamps) [R3][R4], ybar = T(x / max(rho, eps)):
+//   ybar >= 0 : code = h + m,        m = #{i >= 1 : ybar >= tau_i}
+//   ybar <  0 : code = h - 1 - m,    m = #{i >= 1 : |ybar| > tau_i}
+// The kernels rotate the raw row, y = T(x), and compare against per-row
+// thresholds r*tau_i with r = max(rho, eps): ybar >= tau <=> y >= r*tau
+// (T is linear and r > 0) [R14c].  For positive floats |y| > a <=>
+// nextdown(|y|) >= a, and for y < 0, nextdown(|y|) = y * (-1 + 2^-24) exactly
+// (round to nearest), while for y >= 0 that product is <= 0; so
+// key = max(y, y * (-1 + 2^-24)) turns both cases into key >= r*tau.  With
+// m < h: h + m = m ^ h and h - 1 - m = m ^ (h - 1), so code = m ^ (h - s),
+// s the sign bit.  Decisions are taken in fp32, the kernel's precision.
+//
+// Per-row quantizer constants for a pair of rows (row A in .x, row B in .y).
+template <int BITS>
+struct RowQ {
+  static constexpr int H = 1 << (BITS - 1);
+  float2 thr[H];   // thr[i] = r * tau_i, i >= 1
+  float2 c0;       // rho * cpos[0]
+  float2 dl[H];    // dl[i] = rho * delta_i, i >= 1
+};
+
+template <int BITS, bool VALUE>
+__device__ __forceinline__ void make_rowq(RowQ<BITS>& q, float2 rho, const KCodebook& cb) {
+  constexpr int H = 1 << (BITS - 1);
+  const float2 r = f2(fmaxf(rho.x, 1e-12f), fmaxf(rho.y, 1e-12f));   // max(rho, eps) [R5]
+#pragma unroll
+  for (int i = 1; i < H; ++i) q.thr[i] = mul2(r, bc(cb.tau[i]));
+  if (VALUE) {
+    q.c0 = mul2(rho, bc(cb.cpos[0]));
+#pragma unroll
+    for (int i = 1; i < H; ++i) q.dl[i] = mul2(rho, bc(cb.delta[i]));
+  }
 }
+
 __device__ __forceinline__ float sign_xor(float c, float y) {
   return __uint_as_float(__float_as_uint(c) ^ (__float_as_uint(y) & 0x80000000u));
 }
 
-// One coordinate pair through Q.  Returns the signed centroids (both rows);
-// with CODES also the two codes.  The centroid is accumulated as
-// cpos[0] + sum_i [key >= tau_i] * delta_i with fp32 steps chosen on the host
-// so that the chain lands exactly on C[code] (see params.cpp).
-template <int BITS, bool CODES>
-__device__ __forceinline__ float2 quantize_pair(float2 y, const KCodebook& cb, uint32_t& code_a,
+// One coordinate pair through Q.  VALUE: returns rho * (signed centroid),
+// accumulated as rho*cpos[0] + sum_i [key >= r*tau_i] * rho*delta_i.  CODE:
+// the two codes (count in the low mantissa bits of 2^23 + sum of indicators).
+template <int BITS, bool VALUE, bool CODE>
+__device__ __forceinline__ float2 quantize_pair(float2 y, const RowQ<BITS>& q, uint32_t& code_a,
                                                 uint32_t& code_b) {
   constexpr int H = 1 << (BITS - 1);
-  const uint32_t sa = sbit(y.x), sb = sbit(y.y);
-  const float ka = key_of(y.x, sa), kb = key_of(y.y, sb);
-  float2 c = bc(cb.cpos[0]);
-  float2 m = bc(8388608.0f);  // 2^23: the count lands in the low mantissa bits
+  const float2 ny = mul2(y, bc(-1.0f + 5.9604644775390625e-8f));   // -1 + 2^-24
+  const float ka = fmaxf(y.x, ny.x), kb = fmaxf(y.y, ny.y);
+  float2 c = q.c0;
+  float2 m = bc(8388608.0f);  // 2^23
 #pragma unroll
   for (int i = 1; i < H; ++i) {
-    const float2 g = f2(ka >= cb.tau[i] ? 1.0f : 0.0f, kb >= cb.tau[i] ? 1.0f : 0.0f);
-    c = fma2(g, bc(cb.delta[i]), c);
-    if (CODES) m = add2(m, g);
+    const float2 g = f2(ka >= q.thr[i].x ? 1.0f : 0.0f, kb >= q.thr[i].y ? 1.0f : 0.0f);
+    if (VALUE) c = fma2(g, q.dl[i], c);
+    if (CODE) m = add2(m, g);
   }
-  if (CODES) {
+  if (CODE) {
+    const uint32_t sa = __float_as_uint(y.x) >> 31, sb = __float_as_uint(y.y) >> 31;
     code_a = (__float_as_uint(m.x) ^ (uint32_t)(H - (int)sa)) & (2u * H - 1u);
     code_b = (__float_as_uint(m.y) ^ (uint32_t)(H - (int)sb)) & (2u * H - 1u);
   }
-  return f2(sign_xor(c.x, y.x), sign_xor(c.y, y.y));
+  if (VALUE) return f2(sign_xor(c.x, y.x), sign_xor(c.y, y.y));
+  return c;
+}
+
+// Same decision on a normalised pair (ybar = T(xbar)) against the codebook as
+// stored (constant-bank operands, no per-row registers): centroid values are
+// unscaled, the caller multiplies by rho after T^-1.
+template <int BITS, bool VALUE, bool CODE>
+__device__ __forceinline__ float2 quantize_pair_u(float2 y, const KCodebook& cb, uint32_t& code_a,
+                                                  uint32_t& code_b) {
+  constexpr int H = 1 << (BITS - 1);
+  const float2 ny = mul2(y, bc(-1.0f + 5.9604644775390625e-8f));
+  const float ka = fmaxf(y.x, ny.x), kb = fmaxf(y.y, ny.y);
+  float2 c = bc(cb.cpos[0]);
+  float2 m = bc(8388608.0f);
+#pragma unroll
+  for (int i = 1; i < H; ++i) {
+    const float2 g = f2(ka >= cb.tau[i] ? 1.0f : 0.0f, kb >= cb.tau[i] ? 1.0f : 0.0f);
+    if (VALUE) c = fma2(g, bc(cb.delta[i]), c);
+    if (CODE) m = add2(m, g);
+  }
+  if (CODE) {
+    const uint32_t sa = __float_as_uint(y.x) >> 31, sb = __float_as_uint(y.y) >> 31;
+    code_a = (__float_as_uint(m.x) ^ (uint32_t)(H - (int)sa)) & (2u * H - 1u);
+    code_b = (__float_as_uint(m.y) ^ (uint32_t)(H - (int)sb)) & (2u * H - 1u);
+  }
+  if (VALUE) return f2(sign_xor(c.x, y.x), sign_xor(c.y, y.y));
+  return c;
 }
 
 // ------------------------------------------------------------- bit packing
@@ -347,10 +387,10 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 }
 
 // --------------------------------------------------------- encoder (K1/K3)
-// MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y; codes and
-// norms too when `codes` is non-null).
+// MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y only).
+// MODE 2: fused roundtrip that also writes codes and norms.
 template <class T, int D, int BITS, int VAR, int MODE>
-__global__ void __launch_bounds__(kCtaThreads)
+__global__ void __launch_bounds__(kCtaThreads, Geo<T, D, BITS, VAR>::MIN_CTAS)
 k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x, T* y,
          uint8_t* __restrict__ codes, float* __restrict__ norms) {
   using Gm = Geo<T, D, BITS, VAR>;
@@ -374,7 +414,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        mbar_wait_backoff(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], ph ^ 1);
         const int64_t v0 = t * TILE_V;
         const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
         const uint32_t bytes = (uint32_t)(nv * Gm::ROWB);
@@ -392,32 +432,38 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   const int vslot = lane / G;
   float P[NBL][PW * PW];
   load_ops<Gm>(mat, sub, P);
-  const bool emit = (MODE == 0) || (codes != nullptr);
+  constexpr bool emit = MODE != 1;
+  constexpr bool value = MODE != 0;
 
   int s = 0;
   uint32_t ph = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&full[s], ph);
     const uint8_t* st = smem + s * STAGE;
-    uint4 raw[U][CPL];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int vl = (warp * U + u) * VPW + vslot;  // row within the tile
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) raw[u][i] = lds128(st + vl * Gm::ROWB + (sub + i * G) * 16);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // stage may be refilled
+    const int ss_ = s;
     if (++s == NST) { s = 0; ph ^= 1; }
 
+    // one pair of rows at a time (rows u in .x, u+1 in .y): keeps the live
+    // state of a single pair in registers so two CTAs fit per SM
+#pragma unroll 1
+    for (int u = 0; u < U; u += 2) {
+      uint4 ra[CPL], rb[CPL];
+      const int vl = (warp * U + u) * VPW + vslot;   // row within the tile
 #pragma unroll
-    for (int u = 0; u < U; u += 2) {  // rows u (.x) and u+1 (.y)
-      const int64_t va = t * TILE_V + (warp * U + u) * VPW + vslot;
+      for (int i = 0; i < CPL; ++i) {
+        ra[i] = lds128(st + vl * Gm::ROWB + (sub + i * G) * 16);
+        rb[i] = lds128(st + (vl + VPW) * Gm::ROWB + (sub + i * G) * 16);
+      }
+      if (u + 2 == U) {                                // last rows read: release the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[ss_]);
+      }
+      const int64_t va = t * TILE_V + vl;
       const int64_t vb = va + VPW;
       float2 v[EPL];
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) to_pairs<T>(raw[u][i], raw[u + 1][i], v + i * EPC);
-      // Alg.1 l.1: rho = ||x||, xbar = x / max(rho, eps)  [R5]
+      for (int i = 0; i < CPL; ++i) to_pairs<T>(ra[i], rb[i], v + i * EPC);
+      // Alg.1 l.1: rho = ||x||_2
       float2 ss = mul2(v[0], v[0]);
 #pragma unroll
       for (int e = 1; e < EPL; ++e) ss = fma2(v[e], v[e], ss);
@@ -425,7 +471,17 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       for (int o = G / 2; o >= 1; o >>= 1)
         ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
       const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
-      const float2 inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));
+      // SCALED: compare y = T(x) with per-row thresholds r*tau (saves the
+      // normalisation and the final rescale); otherwise (register-heavy
+      // b=4 / code-emitting variants) normalise x and use the codebook as is.
+      constexpr bool SCALED = MODE == 0 || BITS <= (MODE == 1 ? 3 : 2);
+      RowQ<BITS> q;
+      float2 inv = bc(1.0f);
+      if constexpr (SCALED) {
+        make_rowq<BITS, value>(q, rho, cb);
+      } else {
+        inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
+      }
 
       float2 out[EPL];
       uint32_t cwa[CPL], cwb[CPL];
@@ -433,33 +489,41 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
 #pragma unroll
       for (int b = 0; b < NBL; ++b) {
-        float2 xb[PW], yb[PW], cq[PW];
+        float2 yb[PW], cq[PW];
+        if constexpr (SCALED) {
+          rot_fwd<PW>(P[b], v + b * PW, yb);             // y = T(x)  (Alg.1 l.5/9/13, [R14c])
+        } else {
+          float2 xb[PW];
 #pragma unroll
-        for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);
-        rot_fwd<PW>(P[b], xb, yb);                       // v~ = T(v)     (Alg.1 l.5/9/13)
+          for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
+          rot_fwd<PW>(P[b], xb, yb);                     // v~ = T(xbar)
+        }
 #pragma unroll
         for (int j = 0; j < PW; ++j) {
           const int lc = b * PW + j;                     // lane coordinate
           if (emit) {
             uint32_t ca, cb2;
-            cq[j] = quantize_pair<BITS, true>(yb[j], cb, ca, cb2);   // v^ = Q(v~)
+            if constexpr (SCALED) cq[j] = quantize_pair<BITS, value, true>(yb[j], q, ca, cb2);   // v^ = Q(v~)
+            else cq[j] = quantize_pair_u<BITS, value, true>(yb[j], cb, ca, cb2);
             cwa[lc / EPC] |= ca << ((lc % EPC) * BITS);
             cwb[lc / EPC] |= cb2 << ((lc % EPC) * BITS);
           } else {
-            uint32_t dummy0, dummy1;
-            cq[j] = quantize_pair<BITS, false>(yb[j], cb, dummy0, dummy1);
+            uint32_t d0, d1;
+            if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
+            else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
           }
         }
-        if (MODE == 1) {
-          float2 rb[PW];
-          rot_inv<PW>(P[b], cq, rb);                     // v_rec = T^-1(v^)
+        if (value) {
+          rot_inv<PW>(P[b], cq, out + b * PW);           // x^ = T^-1(rho * v^)  (l.7/11/15)
+          if constexpr (!SCALED) {
 #pragma unroll
-          for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(rb[j], rho);   // x^ = rho * v_rec
+            for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
+          }
         }
       }
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
-        if (MODE == 1) {
+        if (value) {
           uint4 oa, ob;
           from_pairs<T>(out + i * EPC, oa, ob);
           const size_t off = (size_t)(sub + i * G) * EPC;
@@ -485,6 +549,13 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 
 // ---------------------------------------------------------------- decoder (K2)
 // Ring stage = TILE_V rows of packed codes (RB bytes each) + their norms.
+// One row per lane group at a time; coordinates are processed in adjacent
+// pairs (e, e+1) so the inverse rotation is v_(j,j+1) = sum_i
+// (M_ij, M_i,j+1) * c_i: row pairs of the row-major operator times a
+// broadcast centroid, and the fp16 pack takes (v_j, v_j+1) as is.  The
+// centroid lookup C[code] is a warp shuffle from a register table
+// (lane k of every aligned group of L lanes holds C[k]); the shuffle's
+// width-L source index does the masking of the code field.
 template <class T, int D, int BITS, int VAR>
 __global__ void __launch_bounds__(kCtaThreads)
 k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
@@ -492,16 +563,14 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
   using Gm = Geo<T, D, BITS, VAR>;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
   constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
-  constexpr int B = Gm::B, W = Gm::W, RB = Gm::RB;
+  constexpr int B = Gm::B, RB = Gm::RB;
   constexpr int STAGE = Gm::DEC_STAGE, NST = Gm::DEC_STAGES, CODES_B = Gm::DEC_CODES;
   constexpr int L = 1 << BITS;
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
   uint64_t* empty = full + NST;
-  float* s_cent = reinterpret_cast<float*>(empty + NST);
   ring_init<NST>(full, empty);
-  if (threadIdx.x < L) s_cent[threadIdx.x] = cb.cent[threadIdx.x];
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -513,14 +582,12 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        mbar_wait_backoff(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], ph ^ 1);
         const int64_t v0 = t * TILE_V;
         const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
-        const uint32_t cbytes = (uint32_t)(nv * RB), nbytes = (uint32_t)(nv * 4);
-        // bulk copies need 16-byte sizes: round up inside the row arrays only
-        // when the rounded range stays within the caller's buffers (the tail
-        // tile rounds down and the remainder is read directly, see below).
-        const uint32_t c16 = cbytes & ~15u, n16 = nbytes & ~15u;
+        // bulk copies move whole 16-byte units; a ragged tail of the codes or
+        // norms arrays is read directly from global memory by the consumers
+        const uint32_t c16 = (uint32_t)(nv * RB) & ~15u, n16 = (uint32_t)(nv * 4) & ~15u;
         if (c16 + n16 == 0) {
           mbar_arrive(&full[s]);
         } else {
@@ -538,6 +605,7 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
   const int vslot = lane / G;
   float P[NBL][PW * PW];
   load_ops<Gm>(mat, sub, P);
+  const float ctab = cb.cent[lane & (L - 1)];   // C[k] in lane k of each group of L
 
   int s = 0;
   uint32_t ph = 0;
@@ -546,63 +614,90 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
     const uint8_t* st = smem + s * STAGE;
     const int64_t v0 = t * TILE_V;
     const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;
-    const int64_t c16 = (nv * RB) & ~(int64_t)15, n16 = (nv * 4) & ~(int64_t)15;
     uint32_t bits[U][CPL];
     float rho[U];
+    if (nv == TILE_V && ((TILE_V * RB) % 16 == 0)) {   // full tile: everything is in smem
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int vl = (warp * U + u) * VPW + vslot;
-      const bool valid = vl < nv;
+      for (int u = 0; u < U; ++u) {
+        const int vl = (warp * U + u) * VPW + vslot;
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        // this lane's B bits start at bit (i*G + sub)*B of the row
-        const int bit0 = (i * G + sub) * B;
-        const int byte0 = vl * RB + (bit0 >> 5) * 4;
-        const int sh = bit0 & 31;
-        uint32_t lo = 0, hi = 0;
-        if (valid) {
-          lo = (byte0 + 4 <= c16) ? lds32(st + byte0) : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0));
-          if (B < 32 && sh + B > 32)
-            hi = (byte0 + 8 <= c16) ? lds32(st + byte0 + 4)
-                                    : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0 + 4));
+        for (int i = 0; i < CPL; ++i) {
+          const int bit0 = (i * G + sub) * B;        // this lane's bits in the row stream
+          const int byte0 = vl * RB + (bit0 >> 5) * 4, sh = bit0 & 31;
+          uint32_t r = lds32(st + byte0);
+          if (B < 32 && sh + B > 32) r = __funnelshift_r(r, lds32(st + byte0 + 4), sh);
+          else if (sh) r >>= sh;
+          bits[u][i] = r;
         }
-        uint32_t r = (sh == 0) ? lo : ((lo >> sh) | (hi << (32 - sh)));
-        if (B < 32) r &= (1u << (B & 31)) - 1u;
-        bits[u][i] = r;
+        rho[u] = ldsf(st + CODES_B + vl * 4);
       }
-      rho[u] = valid ? ((vl * 4 + 4 <= n16) ? ldsf(st + CODES_B + vl * 4) : __ldg(norms + v0 + vl)) : 0.0f;
+    } else {                                           // tail tile: direct loads
+      const int64_t c16 = (nv * RB) & ~(int64_t)15, n16 = (nv * 4) & ~(int64_t)15;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int vl = (warp * U + u) * VPW + vslot;
+        const bool valid = vl < nv;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          const int bit0 = (i * G + sub) * B;
+          const int byte0 = vl * RB + (bit0 >> 5) * 4, sh = bit0 & 31;
+          uint32_t lo = 0, hi = 0;
+          if (valid) {
+            lo = (byte0 + 4 <= c16) ? lds32(st + byte0)
+                                    : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0));
+            if (B < 32 && sh + B > 32)
+              hi = (byte0 + 8 <= c16) ? lds32(st + byte0 + 4)
+                                      : __ldg(reinterpret_cast<const unsigned*>(codes + v0 * RB + byte0 + 4));
+          }
+          bits[u][i] = (B < 32 && sh + B > 32) ? __funnelshift_r(lo, hi, sh) : (lo >> sh);
+        }
+        rho[u] = valid ? ((vl * 4 + 4 <= n16) ? ldsf(st + CODES_B + vl * 4) : __ldg(norms + v0 + vl)) : 0.0f;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == NST) { s = 0; ph ^= 1; }
 
 #pragma unroll
-    for (int u = 0; u < U; u += 2) {
-      const int64_t va = v0 + (warp * U + u) * VPW + vslot;
-      const int64_t vb = va + VPW;
-      const float2 r2 = f2(rho[u], rho[u + 1]);
-      float2 out[EPL];
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + (warp * U + u) * VPW + vslot;
+      const float2 r2 = bc(rho[u]);
+      float2 out[EPL / 2];
 #pragma unroll
       for (int b = 0; b < NBL; ++b) {
-        float2 cq[PW], rb[PW];
+        float c[PW];
 #pragma unroll
         for (int j = 0; j < PW; ++j) {
           const int lc = b * PW + j;
-          const uint32_t ca = (bits[u][lc / EPC] >> ((lc % EPC) * BITS)) & (L - 1);
-          const uint32_t cbb = (bits[u + 1][lc / EPC] >> ((lc % EPC) * BITS)) & (L - 1);
-          cq[j] = f2(s_cent[ca], s_cent[cbb]);            // v^ = C[code]
+          // v^ = C[code]: width-L shuffle masks the BITS-wide field itself
+          c[j] = __shfl_sync(kFull, ctab, (int)(bits[u][lc / EPC] >> ((lc % EPC) * BITS)), L);
         }
-        rot_inv<PW>(P[b], cq, rb);                        // T^-1
 #pragma unroll
-        for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(rb[j], r2);   // x^ = rho * ...
+        for (int jp = 0; jp < PW; jp += 2) {           // T^-1 on coordinate pairs
+          float2 a = mul2(f2(P[b][jp], P[b][jp + 1]), bc(c[0]));
+#pragma unroll
+          for (int i = 1; i < PW; ++i) a = fma2(f2(P[b][PW * i + jp], P[b][PW * i + jp + 1]), bc(c[i]), a);
+          out[(b * PW + jp) / 2] = mul2(a, r2);        // x^ = rho * ...
+        }
       }
+      if (v < n) {
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        uint4 oa, ob;
-        from_pairs<T>(out + i * EPC, oa, ob);
-        const size_t off = (size_t)(sub + i * G) * EPC;
-        if (va < n) st_stream(y + va * D + off, oa);
-        if (vb < n) st_stream(y + vb * D + off, ob);
+        for (int i = 0; i < CPL; ++i) {
+          uint4 o;
+          if constexpr (EPC == 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              __half2 h = __floats2half2_rn(out[i * 4 + k].x, out[i * 4 + k].y);
+              w[k] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            o = make_uint4(w[0], w[1], w[2], w[3]);
+          } else {
+            o = make_uint4(__float_as_uint(out[i * 2].x), __float_as_uint(out[i * 2].y),
+                           __float_as_uint(out[i * 2 + 1].x), __float_as_uint(out[i * 2 + 1].y));
+          }
+          st_stream(y + v * D + (size_t)(sub + i * G) * EPC, o);
+        }
       }
     }
   }
