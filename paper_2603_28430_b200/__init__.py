@@ -28,7 +28,8 @@ FULL, FAST, PLANAR2D = 0, 1, 2
 F32, F16 = 0, 1
 VARIANTS = {"full": FULL, "fast": FAST, "planar2d": PLANAR2D, "2d": PLANAR2D}
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libisoquant.so")
+LIB_PATH = os.environ.get("IQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                         "libisoquant.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -46,8 +46,8 @@ def _newest(paths):
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str, extra: list[str], verbose: bool) -> str:
-    obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+def _compile(src: str, extra: list[str], verbose: bool, objdir: str = OBJDIR) -> str:
+    obj = os.path.join(objdir, os.path.basename(src) + ".o")
     deps = [src] + _headers()
     if os.path.exists(obj) and os.path.getmtime(obj) >= _newest(deps):
         return obj
@@ -62,22 +62,25 @@ def _compile(src: str, extra: list[str], verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | None = None) -> str:
-    """Compile (incrementally) and link libisoquant.so; return its path."""
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | None = None,
+          lib: str = LIB, objdir: str = OBJDIR) -> str:
+    """Compile (incrementally) and link libisoquant.so; return its path.
+    ``extra``/``lib``/``objdir`` build tuning variants (e.g. -DIQ_NWC=7) side by
+    side for experiments; the product is the default build."""
+    os.makedirs(objdir, exist_ok=True)
     extra = list(extra or [])
     srcs = _sources()
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(max_workers=jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra, verbose), srcs))
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static"]
+        objs = list(ex.map(lambda s: _compile(s, extra, verbose, objdir), srcs))
+    if not os.path.exists(lib) or os.path.getmtime(lib) < _newest(objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-cudart", "static"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -33,47 +33,76 @@
 namespace iq {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNWC = 8;                        // compute warps per CTA
-constexpr int kCtaThreads = 32 * (kNWC + 1);   // + 1 producer warp
-constexpr int kRingBytes = 96 * 1024;          // TMA ring per CTA (2 CTAs / SM)
+#ifndef IQ_PAIR_UNROLL
+#define IQ_PAIR_UNROLL 1
+#endif
+constexpr int kPairUnroll = IQ_PAIR_UNROLL;    // row pairs interleaved per iteration
 constexpr int kThreads = 256;                  // statistics kernel CTAs
 
 template <class T> struct DT;
 template <> struct DT<float> { static constexpr int EPC = 4; };
 template <> struct DT<__half> { static constexpr int EPC = 8; };
 
-template <class T, int D, int BITS, int VAR>
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+constexpr int clcm(int a, int b) { return a / cgcd(a, b) * b; }
+
+// Chunks per lane: the smallest power of two giving >= IQ_TPL coordinates
+// per lane (fewer lanes per row = fewer shuffle levels and per-row overhead
+// amortised over more coordinates, at the price of operator registers),
+// bounded so that <= 32 lanes serve a row and a lane group's code bits fill
+// whole 32-bit words.
+#ifndef IQ_TPL
+#define IQ_TPL 8
+#endif
+template <int CHUNKS, int EPC, int BITS>
+constexpr int pick_cpl() {
+  int cpl = 1;
+  while (cpl * EPC < IQ_TPL && cpl * 2 <= CHUNKS) cpl *= 2;
+  while (CHUNKS / cpl > 32) cpl *= 2;
+  while (cpl > 1 && ((CHUNKS / cpl) * EPC * BITS) % 32 != 0) cpl /= 2;
+  return cpl;
+}
+
+// Launch policy (measured on B200): encoders whose
+// per-lane operators fit in 32 registers run one CTA of 16 compute warps
+// with a 200 KB TMA ring; encoders with larger operators (d = 512) one CTA
+// of 8 compute warps; decoders two CTAs of 8 compute warps per SM.
+template <class T, int D, int BITS, int VAR, bool ENC>
 struct Geo {
   static constexpr int EPC = DT<T>::EPC;
   static constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;   // block width
   static constexpr int CHUNKS = D / EPC;
-  static constexpr int G = CHUNKS < 32 ? CHUNKS : 32;              // lanes per row
-  static constexpr int CPL = CHUNKS / G;                           // chunks per lane
+  static constexpr int CPL = pick_cpl<CHUNKS, EPC, BITS>();        // chunks per lane
+  static constexpr int G = CHUNKS / CPL;                           // lanes per row
   static constexpr int VPW = 32 / G;                               // rows per warp
   static constexpr int EPL = CPL * EPC;                            // coordinates per lane
   static constexpr int NBL = EPL / PW;                             // blocks per lane
+  static constexpr bool SMALL_OPS = NBL * PW * PW <= 32;
+  static constexpr int NWC = (ENC && SMALL_OPS) ? 16 : 8;         // compute warps per CTA
+  static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
+  static constexpr int MIN_CTAS = ENC ? 1 : 2;
+  static constexpr int RING = (ENC && SMALL_OPS) ? 200 * 1024 : 96 * 1024;   // TMA ring per CTA
   static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
   static constexpr int RB = D * BITS / 8;                          // code bytes per row
   static constexpr int B = EPC * BITS;                             // code bits per chunk
   static constexpr int W = G * B / 32;                             // code words per segment
   // rows per stage: >= 16 KB of x and a whole number of row pairs per warp
-  static constexpr int TV0 = 16384 / ROWB;
-  static constexpr int TILE_V = TV0 > 2 * kNWC * VPW ? TV0 : 2 * kNWC * VPW;
-  static constexpr int U = TILE_V / (kNWC * VPW);                  // rows per lane group per stage
+  // (granule: whole row pairs per warp, and 16-byte aligned norm tiles)
+  static constexpr int GR = clcm(2 * NWC * VPW, 4);
+  static constexpr int TV0 = (16384 / ROWB) / GR * GR;
+  static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
+  static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
-  static constexpr int ENC_STAGES = (kRingBytes / ENC_STAGE) < 8 ? (kRingBytes / ENC_STAGE) : 8;
+  static constexpr int ENC_STAGES = (RING / ENC_STAGE) < 12 ? (RING / ENC_STAGE) : 12;
   // decoder stage: codes tile (16-B aligned) followed by the norms tile
   static constexpr int DEC_CODES = (TILE_V * RB + 15) / 16 * 16;
-  static constexpr int DEC_STAGE = DEC_CODES + TILE_V * 4;
-  static constexpr int DEC_STAGES = (kRingBytes / DEC_STAGE) < 8 ? (kRingBytes / DEC_STAGE) : 8;
+  static constexpr int DEC_STAGE = (DEC_CODES + TILE_V * 4 + 127) / 128 * 128;
+  static constexpr int DEC_STAGES = (RING / DEC_STAGE) < 8 ? (RING / DEC_STAGE) : 8;
   static_assert(D % EPC == 0 && (G & (G - 1)) == 0 && CHUNKS % G == 0, "unsupported d");
   static_assert(EPL % PW == 0, "lane must own whole blocks");
-  static_assert(U % 2 == 0 && TILE_V % (2 * kNWC * VPW) == 0, "rows pair up");
+  static_assert(U % 2 == 0 && TILE_V % (2 * NWC * VPW) == 0, "rows pair up");
   static_assert((G * B) % 32 == 0, "code segment must be whole words");
   static_assert(ENC_STAGES >= 2 && DEC_STAGES >= 2, "ring too shallow");
-  // 2 CTAs (16 compute warps) per SM when a lane's operators fit (<= 96
-  // registers per thread with 18 warps per SM); 1 CTA for d=512
-  static constexpr int MIN_CTAS = NBL * PW * PW <= 32 ? 2 : 1;
 };
 
 // Shared-memory footprint: ring + full/empty barriers + the centroid table.
@@ -375,12 +404,12 @@ __device__ __forceinline__ void load_ops(const float* __restrict__ mat, int sub,
 }
 
 // Ring setup shared by the three kernels.
-template <int NST>
+template <int NST, int NWC>
 __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNWC);
+      mbar_init(&empty[s], NWC);
     }
     fence_mbar_init();
   }
@@ -390,10 +419,12 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y only).
 // MODE 2: fused roundtrip that also writes codes and norms.
 template <class T, int D, int BITS, int VAR, int MODE>
-__global__ void __launch_bounds__(kCtaThreads, Geo<T, D, BITS, VAR>::MIN_CTAS)
+__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, true>::CTA_THREADS,
+                                  Geo<T, D, BITS, VAR, true>::MIN_CTAS)
 k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x, T* y,
          uint8_t* __restrict__ codes, float* __restrict__ norms) {
-  using Gm = Geo<T, D, BITS, VAR>;
+  using Gm = Geo<T, D, BITS, VAR, true>;
+  constexpr int NWC = Gm::NWC;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
   constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
   constexpr int B = Gm::B, W = Gm::W, RB = Gm::RB;
@@ -402,13 +433,13 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
   uint64_t* empty = full + NST;
-  ring_init<NST>(full, empty);
+  ring_init<NST, NWC>(full, empty);
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + TILE_V - 1) / TILE_V;
 
-  if (warp == kNWC) {  // ---------------- producer: TMA bulk loads into the ring
+  if (warp == NWC) {  // ---------------- producer: TMA bulk loads into the ring
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int s = 0;
@@ -445,7 +476,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 
     // one pair of rows at a time (rows u in .x, u+1 in .y): keeps the live
     // state of a single pair in registers so two CTAs fit per SM
-#pragma unroll 1
+#pragma unroll kPairUnroll
     for (int u = 0; u < U; u += 2) {
       uint4 ra[CPL], rb[CPL];
       const int vl = (warp * U + u) * VPW + vslot;   // row within the tile
@@ -474,7 +505,8 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       // SCALED: compare y = T(x) with per-row thresholds r*tau (saves the
       // normalisation and the final rescale); otherwise (register-heavy
       // b=4 / code-emitting variants) normalise x and use the codebook as is.
-      constexpr bool SCALED = MODE == 0 || BITS <= (MODE == 1 ? 3 : 2);
+      // K1 (MODE 0) and K3+codes (MODE 2) share one rule so they emit identical codes
+      constexpr bool SCALED = BITS <= (MODE == 1 ? 3 : 2);
       RowQ<BITS> q;
       float2 inv = bc(1.0f);
       if constexpr (SCALED) {
@@ -557,10 +589,12 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 // (lane k of every aligned group of L lanes holds C[k]); the shuffle's
 // width-L source index does the masking of the code field.
 template <class T, int D, int BITS, int VAR>
-__global__ void __launch_bounds__(kCtaThreads)
+__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, false>::CTA_THREADS,
+                                  Geo<T, D, BITS, VAR, false>::MIN_CTAS)
 k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
          const uint8_t* __restrict__ codes, const float* __restrict__ norms, T* __restrict__ y) {
-  using Gm = Geo<T, D, BITS, VAR>;
+  using Gm = Geo<T, D, BITS, VAR, false>;
+  constexpr int NWC = Gm::NWC;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
   constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
   constexpr int B = Gm::B, RB = Gm::RB;
@@ -570,13 +604,13 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
   uint64_t* empty = full + NST;
-  ring_init<NST>(full, empty);
+  ring_init<NST, NWC>(full, empty);
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + TILE_V - 1) / TILE_V;
 
-  if (warp == kNWC) {
+  if (warp == NWC) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int s = 0;

@@ -47,9 +47,14 @@ def _parity(variant, dt, d, bits, X, seed=SEED):
     rt = 1e-3 if dt == iq.F16 else 2e-6
     b64 = y.astype(np.float64)
     den = np.maximum(np.linalg.norm(b64, axis=1), 1e-30)
+    # (rows whose rotated coordinate sits within rounding of a threshold may
+    # take the other code in a kernel with a different fp32 evaluation order:
+    # allow <= 0.1% such rows; every kernel's own output is checked against
+    # the oracle below)
     for other in (ydq, y_plain):
         a64 = other.astype(np.float64)
-        assert np.all(np.linalg.norm(a64 - b64, axis=1) <= rt * den + 1e-30)
+        bad = np.linalg.norm(a64 - b64, axis=1) > rt * den + 1e-30
+        assert bad.sum() <= max(1, int(1e-3 * len(bad))), bad.sum()
     r = parity.check(X, po, y, codes, norms, NP[dt])
     parity.assert_parity(r, NP[dt], check_mse=X.shape[0] >= 256)
     return r

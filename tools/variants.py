@@ -1,0 +1,99 @@
+"""Build tuning variants of libisoquant side by side and time them.
+
+  python tools/variants.py build            # here (CPU): compile every variant
+  python tools/variants.py time [--d 128 --bits 3 --dtype f16 --variant full]
+                                            # on the GPU box: time each variant
+
+Variants differ only in compile-time knobs (-DIQ_TPL, -DIQ_PAIR_UNROLL); the product build is the default one.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+VARIANTS = {
+    "base": [],
+    "tpl16": ["-DIQ_TPL=16"],
+    "u2": ["-DIQ_PAIR_UNROLL=2"],
+}
+
+
+def lib_path(name):
+    return os.path.join(ROOT, "paper_2603_28430_b200", "build", f"var_{name}", "libisoquant.so")
+
+
+def build(names):
+    from paper_2603_28430_b200 import _build
+    for name in names:
+        d = os.path.dirname(lib_path(name))
+        _build.build(extra=VARIANTS[name], lib=lib_path(name), objdir=d)
+        print("built", name, flush=True)
+
+
+def time_one(a):
+    import torch
+    import iqsynth
+    import paper_2603_28430_b200 as iq
+    tdt = torch.float16 if a.dtype == "f16" else torch.float32
+    s = 2 if a.dtype == "f16" else 4
+    p = iq.iq_make_params(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
+    xs = [iqsynth.device_unit_vectors(a.n, a.d, 7 + j, tdt, "cuda") for j in range(2)]
+    ys = [torch.empty_like(x) for x in xs]
+    codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
+    norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
+    iq.iq_quantize(p, xs[0], codes, norms)
+    cb = p.code_bytes
+    out = {}
+    for name, fn, bpv in [
+        ("rt", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1]), 2 * a.d * s),
+        ("q", lambda i: iq.iq_quantize(p, xs[i & 1], codes, norms), a.d * s + cb + 4),
+        ("dq", lambda i: iq.iq_dequantize(p, codes, norms, y=ys[i & 1]), a.d * s + cb + 4),
+        ("rte", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], codes=codes, norms=norms),
+         2 * a.d * s + cb + 4),
+    ]:
+        for i in range(5):
+            fn(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(40):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 40 * 1e3
+        out[name] = (round(us, 1), round(a.n * bpv / us / 1e3 / 6525.9, 3))
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["build", "time", "time1"])
+    ap.add_argument("--only", nargs="*", default=list(VARIANTS))
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--dtype", default="f16")
+    ap.add_argument("--variant", default="full")
+    ap.add_argument("--n", type=int, default=1 << 20)
+    a = ap.parse_args()
+    if a.cmd == "build":
+        build(a.only)
+    elif a.cmd == "time1":
+        time_one(a)
+    else:
+        for name in a.only:
+            if not os.path.exists(lib_path(name)):
+                continue
+            env = dict(os.environ, IQ_LIB_PATH=lib_path(name))
+            r = subprocess.run([sys.executable, __file__, "time1", "--d", str(a.d), "--bits", str(a.bits),
+                                "--dtype", a.dtype, "--variant", a.variant, "--n", str(a.n)],
+                               env=env, capture_output=True, text=True)
+            line = (r.stdout.strip().splitlines() or [r.stderr.strip()[-300:]])[-1]
+            print(f"{name:16s} {line}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
