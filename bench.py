@@ -263,6 +263,7 @@ def main():
         _build.build()
     barrier()
     import iqsynth
+    from iqsynth import dist as D
     import paper_2603_28430_b200 as iq
 
     vid = iq.VARIANTS[a.variant]
@@ -271,7 +272,7 @@ def main():
     p = iq.iq_make_params(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=local)
     stream = torch.cuda.current_stream()
     # each rank's shard: its own chunk seeds (weak scaling, no data movement)
-    xs = [iqsynth.device_unit_vectors(a.n, a.d, iqsynth.data_seed(2, 100 * rank + j), tdt, dev)
+    xs = [iqsynth.device_unit_vectors(a.n, a.d, D.shard_seed(2, rank, j), tdt, dev)
           for j in range(2)]
     ys = [torch.empty_like(x) for x in xs]
 
@@ -304,8 +305,14 @@ def main():
     barrier()
     t_end = time.time()
     ms = e0.elapsed_time(e1)
-    ms_max = allreduce([ms], dist.ReduceOp.MAX if world > 1 else None)[0]
     clocks = sampler.stop(t_load0, t_end) if sampler else None
+    # reconstruction sums over every rank's full batch (after timing), then one
+    # combine: MAX of the step time, SUM of the statistics (NCCL at N > 1)
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    for j in range(2):
+        iq.iq_error_sums(p, xs[j], ys[j], sums)
+    ms_max, se_tot, _, cnt_tot = D.combine_stats(ms, *sums.tolist(), 2.0 * a.n * a.d, device=dev)
+    mse = se_tot / cnt_tot
 
     ms_step = ms_max / a.steps
     value = world * a.n / (ms_step / 1e3)
@@ -318,12 +325,6 @@ def main():
                 "kernel": f"k_encode<{a.dtype},{a.d},{a.bits},{a.variant},roundtrip>",
                 "algorithmic_bytes_per_launch": bpl, "peak_source": peak_src}
 
-    # reconstruction MSE over every rank's full batch (after timing)
-    sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    for j in range(2):
-        iq.iq_error_sums(p, xs[j], ys[j], sums)
-    tot = allreduce([*sums.tolist(), 2.0 * a.n * a.d], dist.ReduceOp.SUM if world > 1 else None)
-    mse = tot[0] / tot[2]
 
     out = {
         "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world, "steps": a.steps,

@@ -54,6 +54,9 @@ constexpr int clcm(int a, int b) { return a / cgcd(a, b) * b; }
 #ifndef IQ_TPL
 #define IQ_TPL 8
 #endif
+#ifndef IQ_STAGE_KB
+#define IQ_STAGE_KB 16
+#endif
 template <int CHUNKS, int EPC, int BITS>
 constexpr int pick_cpl() {
   int cpl = 1;
@@ -89,7 +92,7 @@ struct Geo {
   // rows per stage: >= 16 KB of x and a whole number of row pairs per warp
   // (granule: whole row pairs per warp, and 16-byte aligned norm tiles)
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
-  static constexpr int TV0 = (16384 / ROWB) / GR * GR;
+  static constexpr int TV0 = (IQ_STAGE_KB * 1024 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
   static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
@@ -473,6 +476,12 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
     const uint8_t* st = smem + s * STAGE;
     const int ss_ = s;
     if (++s == NST) { s = 0; ph ^= 1; }
+    // per-tile bases: row offsets below stay 32-bit, bounds are tile-local
+    const int64_t v0 = t * TILE_V;
+    const int nv = (n - v0) < TILE_V ? (int)(n - v0) : TILE_V;
+    T* const yt = value ? y + v0 * D : nullptr;
+    uint8_t* const ct = emit ? codes + v0 * RB : nullptr;
+    float* const nt = emit ? norms + v0 : nullptr;
 
     // one pair of rows at a time (rows u in .x, u+1 in .y): keeps the live
     // state of a single pair in registers so two CTAs fit per SM
@@ -489,8 +498,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[ss_]);
       }
-      const int64_t va = t * TILE_V + vl;
-      const int64_t vb = va + VPW;
+      const bool oka = vl < nv, okb = vl + VPW < nv;
       float2 v[EPL];
 #pragma unroll
       for (int i = 0; i < CPL; ++i) to_pairs<T>(ra[i], rb[i], v + i * EPC);
@@ -558,22 +566,23 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
         if (value) {
           uint4 oa, ob;
           from_pairs<T>(out + i * EPC, oa, ob);
-          const size_t off = (size_t)(sub + i * G) * EPC;
-          if (va < n) st_stream(y + va * D + off, oa);
-          if (vb < n) st_stream(y + vb * D + off, ob);
+          const int off = vl * D + (sub + i * G) * EPC;
+          if (oka) st_stream(yt + off, oa);
+          if (okb) st_stream(yt + off + VPW * D, ob);
         }
         if (emit) {
           const uint32_t wa = gather_word<G, B>(cwa[i], sub, vbase);
           const uint32_t wb = gather_word<G, B>(cwb[i], sub, vbase);
           if (sub < W) {
-            if (va < n) *reinterpret_cast<uint32_t*>(codes + va * RB + 4 * (i * W + sub)) = wa;
-            if (vb < n) *reinterpret_cast<uint32_t*>(codes + vb * RB + 4 * (i * W + sub)) = wb;
+            const int off = vl * RB + 4 * (i * W + sub);
+            if (oka) *reinterpret_cast<uint32_t*>(ct + off) = wa;
+            if (okb) *reinterpret_cast<uint32_t*>(ct + off + VPW * RB) = wb;
           }
         }
       }
       if (emit && sub == 0) {
-        if (va < n) norms[va] = rho.x;
-        if (vb < n) norms[vb] = rho.y;
+        if (oka) nt[vl] = rho.x;
+        if (okb) nt[vl + VPW] = rho.y;
       }
     }
   }
