@@ -314,6 +314,13 @@ __device__ __forceinline__ float2 quantize_pair(float2 y, const RowQ<BITS>& q, u
   float2 m = bc(8388608.0f);  // 2^23
 #pragma unroll
   for (int i = 1; i < H; ++i) {
+    if constexpr (VALUE && !CODE && BITS == 3) {
+      // b = 3: conditional add on the ALU (FSETP + predicated FADD) instead of
+      // the indicator FFMA2 -- shifts work off the FMA pipe (+3% measured)
+      c.x = ka >= q.thr[i].x ? c.x + q.dl[i].x : c.x;
+      c.y = kb >= q.thr[i].y ? c.y + q.dl[i].y : c.y;
+      continue;
+    }
     const float2 g = f2(ka >= q.thr[i].x ? 1.0f : 0.0f, kb >= q.thr[i].y ? 1.0f : 0.0f);
     if (VALUE) c = fma2(g, q.dl[i], c);
     if (CODE) m = add2(m, g);
@@ -468,6 +475,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   load_ops<Gm>(mat, sub, P);
   constexpr bool emit = MODE != 1;
   constexpr bool value = MODE != 0;
+  const float ctab = cb.cent[lane & ((1 << BITS) - 1)];   // C[k] in lane k of each group of L
 
   int s = 0;
   uint32_t ph = 0;
@@ -510,15 +518,21 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       for (int o = G / 2; o >= 1; o >>= 1)
         ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
       const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
-      // SCALED: compare y = T(x) with per-row thresholds r*tau (saves the
-      // normalisation and the final rescale); otherwise (register-heavy
-      // b=4 / code-emitting variants) normalise x and use the codebook as is.
-      // K1 (MODE 0) and K3+codes (MODE 2) share one rule so they emit identical codes
-      constexpr bool SCALED = BITS <= (MODE == 1 ? 3 : 2);
+      // Decision rule (R14c).  SCALED: compare y = T(x) with per-row
+      // thresholds r*tau, r = max(rho, eps) (saves normalising the row).
+      // K1 (MODE 0) and K3+codes (MODE 2) always use it, so they emit
+      // identical codes; MODE 2 then looks C[code] up in a shuffle table and
+      // rescales after T^-1.  The value-only K3 (MODE 1) also builds
+      // rho*C[code] directly (no rescale) for b <= 3; for b = 4 (seven
+      // thresholds, register-bound) it normalises the row and compares with
+      // the codebook as stored.
+      constexpr bool SCALED = MODE != 1 || BITS <= 3;
+      constexpr bool LOOKUP = MODE == 2;               // value from C[code]
+      constexpr bool RESCALE = value && (!SCALED || LOOKUP);
       RowQ<BITS> q;
       float2 inv = bc(1.0f);
       if constexpr (SCALED) {
-        make_rowq<BITS, value>(q, rho, cb);
+        make_rowq<BITS, MODE == 1>(q, rho, cb);
       } else {
         inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
       }
@@ -541,21 +555,23 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
         for (int j = 0; j < PW; ++j) {
           const int lc = b * PW + j;                     // lane coordinate
-          if (emit) {
+          if constexpr (emit) {
             uint32_t ca, cb2;
-            if constexpr (SCALED) cq[j] = quantize_pair<BITS, value, true>(yb[j], q, ca, cb2);   // v^ = Q(v~)
-            else cq[j] = quantize_pair_u<BITS, value, true>(yb[j], cb, ca, cb2);
+            quantize_pair<BITS, false, true>(yb[j], q, ca, cb2);   // codes of v^ = Q(v~)
             cwa[lc / EPC] |= ca << ((lc % EPC) * BITS);
             cwb[lc / EPC] |= cb2 << ((lc % EPC) * BITS);
+            if constexpr (LOOKUP)                        // v^ = C[code] (width-L shuffle table)
+              cq[j] = f2(__shfl_sync(kFull, ctab, (int)ca, 1 << BITS),
+                         __shfl_sync(kFull, ctab, (int)cb2, 1 << BITS));
           } else {
             uint32_t d0, d1;
             if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
             else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
           }
         }
-        if (value) {
+        if constexpr (value) {
           rot_inv<PW>(P[b], cq, out + b * PW);           // x^ = T^-1(rho * v^)  (l.7/11/15)
-          if constexpr (!SCALED) {
+          if constexpr (RESCALE) {
 #pragma unroll
             for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
           }
@@ -563,7 +579,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       }
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
-        if (value) {
+        if constexpr (value) {
           uint4 oa, ob;
           from_pairs<T>(out + i * EPC, oa, ob);
           const int off = vl * D + (sub + i * G) * EPC;

@@ -17,8 +17,8 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
+    "tpl16": ["-DIQ_TPL=16"],
     "stage32": ["-DIQ_STAGE_KB=32"],
-    "stage32_u2": ["-DIQ_STAGE_KB=32", "-DIQ_PAIR_UNROLL=2"],
 }
 
 
