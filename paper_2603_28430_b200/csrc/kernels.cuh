@@ -360,6 +360,49 @@ __device__ __forceinline__ float2 quantize_pair_u(float2 y, const KCodebook& cb,
   return c;
 }
 
+// Codes of one 16-byte chunk (EPC coordinates) for a pair of rows, formed
+// positionally: with m_e = #{i : key_e >= r*tau_i} and s_e the sign bit, the
+// code is m_e ^ (h - s_e) (see above), so the chunk's LSB-first code word is
+// M ^ (C - S) with M = sum_e m_e 2^(e*BITS), S = sum_e s_e 2^(e*BITS),
+// C = sum_e h 2^(e*BITS) (digit-wise, no carries: m_e < h, s_e <= 1 <= h).
+// M and S are accumulated exactly in fp32 as 2^23 + sum of indicator *
+// 2^(position) with FFMA2 (A coordinates per accumulator keep the sum below
+// 2^23), then read back from the mantissa bits.
+template <int BITS, int EPC>
+__device__ __forceinline__ void encode_chunk(const float2* y, const RowQ<BITS>& q, uint32_t& wa,
+                                             uint32_t& wb) {
+  constexpr int H = 1 << (BITS - 1);
+  constexpr int A = (BITS >= 3) ? 4 : EPC;             // coordinates per accumulator
+  constexpr int NACC = EPC / A;
+  float2 macc[NACC], sacc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) macc[k] = sacc[k] = bc(8388608.0f);
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) {
+    const float w = (float)(1u << ((e % A) * BITS));
+    const float2 ny = mul2(y[e], bc(-1.0f + 5.9604644775390625e-8f));   // key (see quantize_pair)
+    const float ka = fmaxf(y[e].x, ny.x), kb = fmaxf(y[e].y, ny.y);
+#pragma unroll
+    for (int i = 1; i < H; ++i)
+      macc[e / A] = fma2(f2(ka >= q.thr[i].x ? 1.0f : 0.0f, kb >= q.thr[i].y ? 1.0f : 0.0f), bc(w),
+                         macc[e / A]);
+    sacc[e / A] = fma2(f2(y[e].x < 0.0f ? 1.0f : 0.0f, y[e].y < 0.0f ? 1.0f : 0.0f), bc(w), sacc[e / A]);
+  }
+  uint32_t ma = 0, mb = 0, sa = 0, sb = 0;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) {
+    ma |= (__float_as_uint(macc[k].x) - 0x4B000000u) << (k * A * BITS);
+    mb |= (__float_as_uint(macc[k].y) - 0x4B000000u) << (k * A * BITS);
+    sa |= (__float_as_uint(sacc[k].x) - 0x4B000000u) << (k * A * BITS);
+    sb |= (__float_as_uint(sacc[k].y) - 0x4B000000u) << (k * A * BITS);
+  }
+  uint32_t c = 0;
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) c |= (uint32_t)H << (e * BITS);
+  wa = ma ^ (c - sa);
+  wb = mb ^ (c - sb);
+}
+
 // ------------------------------------------------------------- bit packing
 // A lane's chunk contributes B = EPC*BITS consecutive bits of the row's
 // LSB-first bitstream [R7].  G lanes form a segment of G*B bits = W words.
@@ -527,8 +570,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       // thresholds, register-bound) it normalises the row and compares with
       // the codebook as stored.
       constexpr bool SCALED = MODE != 1 || BITS <= 3;
-      constexpr bool LOOKUP = MODE == 2;               // value from C[code]
-      constexpr bool RESCALE = value && (!SCALED || LOOKUP);
+      constexpr bool RESCALE = value && !SCALED;
       RowQ<BITS> q;
       float2 inv = bc(1.0f);
       if constexpr (SCALED) {
@@ -541,39 +583,52 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       uint32_t cwa[CPL], cwb[CPL];
 #pragma unroll
       for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
+      if constexpr (!emit) {                             // K3: values only
 #pragma unroll
-      for (int b = 0; b < NBL; ++b) {
-        float2 yb[PW], cq[PW];
-        if constexpr (SCALED) {
-          rot_fwd<PW>(P[b], v + b * PW, yb);             // y = T(x)  (Alg.1 l.5/9/13, [R14c])
-        } else {
-          float2 xb[PW];
-#pragma unroll
-          for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
-          rot_fwd<PW>(P[b], xb, yb);                     // v~ = T(xbar)
-        }
-#pragma unroll
-        for (int j = 0; j < PW; ++j) {
-          const int lc = b * PW + j;                     // lane coordinate
-          if constexpr (emit) {
-            uint32_t ca, cb2;
-            quantize_pair<BITS, false, true>(yb[j], q, ca, cb2);   // codes of v^ = Q(v~)
-            cwa[lc / EPC] |= ca << ((lc % EPC) * BITS);
-            cwb[lc / EPC] |= cb2 << ((lc % EPC) * BITS);
-            if constexpr (LOOKUP)                        // v^ = C[code] (width-L shuffle table)
-              cq[j] = f2(__shfl_sync(kFull, ctab, (int)ca, 1 << BITS),
-                         __shfl_sync(kFull, ctab, (int)cb2, 1 << BITS));
+        for (int b = 0; b < NBL; ++b) {
+          float2 yb[PW], cq[PW];
+          if constexpr (SCALED) {
+            rot_fwd<PW>(P[b], v + b * PW, yb);           // y = T(x)  (Alg.1 l.5/9/13, [R14c])
           } else {
+            float2 xb[PW];
+#pragma unroll
+            for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
+            rot_fwd<PW>(P[b], xb, yb);                   // v~ = T(xbar)
+          }
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
             uint32_t d0, d1;
             if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
             else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
           }
-        }
-        if constexpr (value) {
           rot_inv<PW>(P[b], cq, out + b * PW);           // x^ = T^-1(rho * v^)  (l.7/11/15)
           if constexpr (RESCALE) {
 #pragma unroll
             for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
+          }
+        }
+      } else {                                           // K1 / K3+codes
+        constexpr int BPCH = EPC / PW;                   // blocks per chunk
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          float2 yb[EPC];
+#pragma unroll
+          for (int bb = 0; bb < BPCH; ++bb)
+            rot_fwd<PW>(P[i * BPCH + bb], v + i * EPC + bb * PW, yb + bb * PW);   // y = T(x)
+          encode_chunk<BITS, EPC>(yb, q, cwa[i], cwb[i]);                       // codes of Q(y)
+          if constexpr (value) {
+            float2 cq[EPC];
+#pragma unroll
+            for (int e = 0; e < EPC; ++e)                // v^ = C[code], width-L shuffle table
+              cq[e] = f2(__shfl_sync(kFull, ctab, (int)(cwa[i] >> (e * BITS)), 1 << BITS),
+                         __shfl_sync(kFull, ctab, (int)(cwb[i] >> (e * BITS)), 1 << BITS));
+#pragma unroll
+            for (int bb = 0; bb < BPCH; ++bb) {
+              float2* o = out + i * EPC + bb * PW;
+              rot_inv<PW>(P[i * BPCH + bb], cq + bb * PW, o);   // T^-1
+#pragma unroll
+              for (int j = 0; j < PW; ++j) o[j] = mul2(o[j], rho);   // x^ = rho * ...
+            }
           }
         }
       }
