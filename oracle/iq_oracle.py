@@ -274,15 +274,22 @@ def make_codebook(d: int, bits: int) -> Codebook:
 
 
 def quantize_codes(y: np.ndarray, cb: Codebook) -> np.ndarray:
-    """Nearest-centroid code of every coordinate (v^ = Q(v~)):
-    code = #{k : y >= t_k} — ties go to the upper code, values beyond the
-    extreme thresholds clamp to the end codes [R3][R4].  The
+    """Nearest-centroid code of every coordinate (v^ = Q(v~)).  The
+    paper does not say how a value exactly half-way between two centroids
+    is coded; reading [R3]: the tie goes to the centroid of LARGER MAGNITUDE
+    (away from zero), and y = +-0 codes on the positive side, so the
+    quantizer of a symmetric codebook is odd: Q(-y) = -Q(y) for y != 0.
+    With the sorted thresholds t_k (midpoints of adjacent centroids):
+        y >= 0 : code = #{k : y >= t_k}
+        y <  0 : code = #{k : y >  t_k}
+    Values beyond the extreme thresholds clamp to the end codes [R4].  The
     decision is taken in fp32, the kernel's precision [R14b]: y is rounded to
     fp32 and compared with the fp32 thresholds."""
     y32 = np.asarray(y).astype(np.float32)
+    nonneg = y32 >= 0
     codes = np.zeros(y32.shape, dtype=np.int64)
     for t in cb.thresholds:
-        codes += (y32 >= t)
+        codes += np.where(nonneg, y32 >= t, y32 > t)
     return codes
 
 

@@ -80,15 +80,31 @@ def test_spec_quantizer_examples():
         assert int(O.quantize_codes(np.array([c["v"]]), cb)[0]) == c["code"]
 
 
-def test_ties_go_up_and_signed_zero():
+def test_ties_away_from_zero_and_signed_zero():
+    """[R3]: a value exactly on a threshold takes the larger-magnitude
+    centroid; +-0 code on the positive side."""
     cb = O.make_codebook(128, 3)
-    T = cb.thresholds
+    T = cb.thresholds                                                    # t_0..t_6, t_3 = 0
     codes = O.quantize_codes(T.astype(np.float64), cb)
-    assert np.array_equal(codes, np.arange(1, 8))                       # y == t_k -> upper
+    assert np.array_equal(codes, [0, 1, 2, 4, 5, 6, 7])                 # t_k<0 -> k, t_k>=0 -> k+1
     assert O.quantize_codes(np.array([0.0, -0.0]), cb).tolist() == [4, 4]   # +-0 -> upper half
     assert O.quantize_codes(np.array([-1e9, 1e9]), cb).tolist() == [0, 7]   # clamp
-    below = np.nextafter(T, -np.inf, dtype=np.float32).astype(np.float64)
-    assert np.array_equal(O.quantize_codes(below, cb), np.arange(0, 7))
+    toward0 = np.where(T < 0, np.nextafter(T, np.inf, dtype=np.float32),
+                       np.nextafter(T, -np.inf, dtype=np.float32)).astype(np.float64)
+    assert np.array_equal(O.quantize_codes(toward0, cb), [1, 2, 3, 3, 4, 5, 6])
+
+
+def test_quantizer_is_odd():
+    """Q(-y) = -Q(y) for y != 0, ties included (symmetric codebook [R2])."""
+    rng = np.random.default_rng(11)
+    for b in (1, 2, 3, 4):
+        cb = O.make_codebook(256, b)
+        y = np.concatenate([(rng.standard_normal(5000) * 0.08).astype(np.float32).astype(np.float64),
+                            cb.thresholds.astype(np.float64)])
+        y = y[y != 0]
+        qp = O.dequantize_codes(O.quantize_codes(y, cb), cb)
+        qn = O.dequantize_codes(O.quantize_codes(-y, cb), cb)
+        assert np.array_equal(qn, -qp)
 
 
 def test_nearest_centroid_brute_force():
