@@ -44,8 +44,10 @@
  *             bitstream in which bit (j*bits + m) is bit m of coordinate j's
  *             code, byte B holding stream bits 8B..8B+7 from its LSB up.
  *             A code is the index k in [0, 2^bits) of the centroid C_k
- *             (C ascending): code = #{k : y >= t_k} (ties go to the upper
- *             code; out-of-range values clamp), y the rotated coordinate.
+ *             (C ascending) nearest to the rotated normalised coordinate y:
+ *             code = #{k : y >= t_k} for y >= 0 and #{k : y > t_k} for y < 0
+ *             (a tie takes the larger-magnitude centroid, +-0 the positive
+ *             side; out-of-range values clamp) — DESIGN.md reading R3.
  *  - norms  : [n] float, rho = ||x||_2 computed in fp32 (stored as is, not
  *             max(rho, eps)).
  */

@@ -262,18 +262,16 @@ __device__ __forceinline__ void rot_inv(const float* M, const float2* c, float2*
 }
 
 // --------------------------------------------------------------- quantizer Q
-// code = #{k : ybar >= t_k} over the symmetric fp32 thresholds (ties go up,
-// out-of-range clamps) [R3][R4], ybar = T(x / max(rho, eps)):
-//   ybar >= 0 : code = h + m,        m = #{i >= 1 : ybar >= tau_i}
-//   ybar <  0 : code = h - 1 - m,    m = #{i >= 1 : |ybar| > tau_i}
-// The kernels rotate the raw row, y = T(x), and compare against per-row
-// thresholds r*tau_i with r = max(rho, eps): ybar >= tau <=> y >= r*tau
-// (T is linear and r > 0) [R14c].  For positive floats |y| > a <=>
-// nextdown(|y|) >= a, and for y < 0, nextdown(|y|) = y * (-1 + 2^-24) exactly
-// (round to nearest), while for y >= 0 that product is <= 0; so
-// key = max(y, y * (-1 + 2^-24)) turns both cases into key >= r*tau.  With
-// m < h: h + m = m ^ h and h - 1 - m = m ^ (h - 1), so code = m ^ (h - s),
-// s the sign bit.  Decisions are taken in fp32, the kernel's precision.
+// Nearest-centroid code over the symmetric fp32 codebook [R1][R2]; a tie
+// takes the larger-magnitude centroid and +-0 the positive side [R3];
+// out-of-range values clamp [R4]; ybar = T(x / max(rho, eps)):
+//   code = h + m (ybar >= 0)  or  h - 1 - m (ybar < 0),  m = #{i >= 1 : |ybar| >= tau_i}
+// The kernels rotate the raw row, y = T(x), and compare |y| with per-row
+// thresholds r*tau_i, r = max(rho, eps): |ybar| >= tau <=> |y| >= r*tau (T is
+// linear, r > 0) [R14c].  |y| is a free operand modifier of the compare.
+// With m < h: h + m = m ^ h and h - 1 - m = m ^ (h - 1), so code = m ^ (h - s),
+// s = [y < 0] (a rotated coordinate is never -0, see rot_fwd).  Decisions are
+// taken in fp32, the kernel's precision [R14b].
 //
 // Per-row quantizer constants for a pair of rows (row A in .x, row B in .y).
 template <int BITS>
@@ -308,8 +306,7 @@ template <int BITS, bool VALUE, bool CODE>
 __device__ __forceinline__ float2 quantize_pair(float2 y, const RowQ<BITS>& q, uint32_t& code_a,
                                                 uint32_t& code_b) {
   constexpr int H = 1 << (BITS - 1);
-  const float2 ny = mul2(y, bc(-1.0f + 5.9604644775390625e-8f));   // -1 + 2^-24
-  const float ka = fmaxf(y.x, ny.x), kb = fmaxf(y.y, ny.y);
+  const float ka = fabsf(y.x), kb = fabsf(y.y);                     // key = |y| [R3]
   float2 c = q.c0;
   float2 m = bc(8388608.0f);  // 2^23
 #pragma unroll
@@ -341,8 +338,7 @@ template <int BITS, bool VALUE, bool CODE>
 __device__ __forceinline__ float2 quantize_pair_u(float2 y, const KCodebook& cb, uint32_t& code_a,
                                                   uint32_t& code_b) {
   constexpr int H = 1 << (BITS - 1);
-  const float2 ny = mul2(y, bc(-1.0f + 5.9604644775390625e-8f));
-  const float ka = fmaxf(y.x, ny.x), kb = fmaxf(y.y, ny.y);
+  const float ka = fabsf(y.x), kb = fabsf(y.y);
   float2 c = bc(cb.cpos[0]);
   float2 m = bc(8388608.0f);
 #pragma unroll
@@ -380,8 +376,7 @@ __device__ __forceinline__ void encode_chunk(const float2* y, const RowQ<BITS>& 
 #pragma unroll
   for (int e = 0; e < EPC; ++e) {
     const float w = (float)(1u << ((e % A) * BITS));
-    const float2 ny = mul2(y[e], bc(-1.0f + 5.9604644775390625e-8f));   // key (see quantize_pair)
-    const float ka = fmaxf(y[e].x, ny.x), kb = fmaxf(y[e].y, ny.y);
+    const float ka = fabsf(y[e].x), kb = fabsf(y[e].y);               // key = |y| [R3]
 #pragma unroll
     for (int i = 1; i < H; ++i)
       macc[e / A] = fma2(f2(ka >= q.thr[i].x ? 1.0f : 0.0f, kb >= q.thr[i].y ? 1.0f : 0.0f), bc(w),
