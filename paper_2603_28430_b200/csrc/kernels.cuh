@@ -46,36 +46,39 @@ template <> struct DT<__half> { static constexpr int EPC = 8; };
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 constexpr int clcm(int a, int b) { return a / cgcd(a, b) * b; }
 
-// Chunks per lane: the smallest power of two giving >= IQ_TPL coordinates
-// per lane (fewer lanes per row = fewer shuffle levels and per-row overhead
-// amortised over more coordinates, at the price of operator registers),
-// bounded so that <= 32 lanes serve a row and a lane group's code bits fill
-// whole 32-bit words.
-#ifndef IQ_TPL
-#define IQ_TPL 8
-#endif
-#ifndef IQ_STAGE_KB
-#define IQ_STAGE_KB 16
-#endif
-template <int CHUNKS, int EPC, int BITS>
+// Chunks per lane: the smallest power of two giving >= TPL coordinates per
+// lane (fewer lanes per row = fewer shuffle levels and less per-row overhead
+// per coordinate, at the price of operator registers), bounded so that <= 32
+// lanes serve a row and a lane group's code bits fill whole 32-bit words.
+template <int CHUNKS, int EPC, int BITS, int TPL>
 constexpr int pick_cpl() {
   int cpl = 1;
-  while (cpl * EPC < IQ_TPL && cpl * 2 <= CHUNKS) cpl *= 2;
+  while (cpl * EPC < TPL && cpl * 2 <= CHUNKS) cpl *= 2;
   while (CHUNKS / cpl > 32) cpl *= 2;
   while (cpl > 1 && ((CHUNKS / cpl) * EPC * BITS) % 32 != 0) cpl /= 2;
   return cpl;
 }
 
-// Launch policy (measured on B200): encoders whose
-// per-lane operators fit in 32 registers run one CTA of 16 compute warps
-// with a 200 KB TMA ring; encoders with larger operators (d = 512) one CTA
-// of 8 compute warps; decoders two CTAs of 8 compute warps per SM.
-template <class T, int D, int BITS, int VAR, bool ENC>
+// Kernel kinds: 0 quantize (K1), 1 fused roundtrip (K3), 2 fused roundtrip +
+// codes, 3 dequantize (K2).  Coordinates per lane (TPL), measured on B200
+// (DESIGN.md section 6): K3 16 except fp16 b = 4 (8); K1 and K3+codes share
+// one geometry so that they emit bit-identical codes and norms: 8 for fp16
+// b <= 3, else 16; the decoder 8.
+template <class T, int BITS, int KIND>
+constexpr int pick_tpl() {
+  constexpr bool f16 = sizeof(T) == 2;
+  if (KIND == 3) return 8;
+  if (KIND == 1) return (f16 && BITS == 4) ? 8 : 16;
+  return (f16 && BITS <= 3) ? 8 : 16;
+}
+
+template <class T, int D, int BITS, int VAR, int KIND>
 struct Geo {
+  static constexpr bool ENC = KIND != 3;
   static constexpr int EPC = DT<T>::EPC;
   static constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;   // block width
   static constexpr int CHUNKS = D / EPC;
-  static constexpr int CPL = pick_cpl<CHUNKS, EPC, BITS>();        // chunks per lane
+  static constexpr int CPL = pick_cpl<CHUNKS, EPC, BITS, pick_tpl<T, BITS, KIND>()>();   // chunks per lane
   static constexpr int G = CHUNKS / CPL;                           // lanes per row
   static constexpr int VPW = 32 / G;                               // rows per warp
   static constexpr int EPL = CPL * EPC;                            // coordinates per lane
@@ -83,7 +86,7 @@ struct Geo {
   static constexpr bool SMALL_OPS = NBL * PW * PW <= 32;
   static constexpr int NWC = (ENC && SMALL_OPS) ? 16 : 8;         // compute warps per CTA
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
-  static constexpr int MIN_CTAS = ENC ? 1 : 2;
+  static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
   static constexpr int RING = (ENC && SMALL_OPS) ? 200 * 1024 : 96 * 1024;   // TMA ring per CTA
   static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
   static constexpr int RB = D * BITS / 8;                          // code bytes per row
@@ -92,7 +95,7 @@ struct Geo {
   // rows per stage: >= 16 KB of x and a whole number of row pairs per warp
   // (granule: whole row pairs per warp, and 16-byte aligned norm tiles)
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
-  static constexpr int TV0 = (IQ_STAGE_KB * 1024 / ROWB) / GR * GR;
+  static constexpr int TV0 = (16384 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
   static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
@@ -129,16 +132,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// Blocking wait: try_wait with a suspend-time hint parks the thread in
-// hardware until the phase completes (no issue slots burnt while waiting).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// One try_wait with a suspend-time hint: the thread is parked in hardware
+// until the phase completes or the hint elapses (no issue slots burnt).
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n.reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Blocking wait.  The retry loop is C++, NOT a branch inside the asm: a
+// suspended try_wait can release the lanes of a warp at different times, and
+// only a compiler-visible loop lets the compiler reconverge the warp before
+// the shuffles that follow (an asm-internal loop leaves it silently diverged).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -467,11 +480,11 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y only).
 // MODE 2: fused roundtrip that also writes codes and norms.
 template <class T, int D, int BITS, int VAR, int MODE>
-__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, true>::CTA_THREADS,
-                                  Geo<T, D, BITS, VAR, true>::MIN_CTAS)
+__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, MODE>::CTA_THREADS,
+                                  Geo<T, D, BITS, VAR, MODE>::MIN_CTAS)
 k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x, T* y,
          uint8_t* __restrict__ codes, float* __restrict__ norms) {
-  using Gm = Geo<T, D, BITS, VAR, true>;
+  using Gm = Geo<T, D, BITS, VAR, MODE>;
   constexpr int NWC = Gm::NWC;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
   constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;
@@ -664,11 +677,11 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 // (lane k of every aligned group of L lanes holds C[k]); the shuffle's
 // width-L source index does the masking of the code field.
 template <class T, int D, int BITS, int VAR>
-__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, false>::CTA_THREADS,
-                                  Geo<T, D, BITS, VAR, false>::MIN_CTAS)
+__global__ void __launch_bounds__(Geo<T, D, BITS, VAR, 3>::CTA_THREADS,
+                                  Geo<T, D, BITS, VAR, 3>::MIN_CTAS)
 k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
          const uint8_t* __restrict__ codes, const float* __restrict__ norms, T* __restrict__ y) {
-  using Gm = Geo<T, D, BITS, VAR, false>;
+  using Gm = Geo<T, D, BITS, VAR, 3>;
   constexpr int NWC = Gm::NWC;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, U = Gm::U;
   constexpr int PW = Gm::PW, NBL = Gm::NBL, EPL = Gm::EPL, TILE_V = Gm::TILE_V;

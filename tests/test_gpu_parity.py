@@ -238,3 +238,20 @@ def test_cfg5_full_d512_b2_fp16_64M_in_place():
     if free < n * 512 * 2 * 1.2:
         pytest.skip("not enough device memory for 64 GiB")
     _large_config(iq.FULL, iq.F16, 512, 2, n, iqsynth.data_seed(5), in_place=True)
+
+
+@pytest.mark.parametrize("d,bits,dt", [(128, 4, iq.F16), (512, 4, iq.F16), (512, 3, iq.F32), (128, 3, iq.F16)])
+def test_norms_over_many_fresh_launches(d, bits, dt):
+    """Regression for a warp-divergence bug: every row's norm from every
+    encoder kernel equals torch's row norm to fp32 rounding, over many fresh
+    launches (each CTA's first TMA stage is where lanes leave the mbarrier
+    wait at different times)."""
+    p = iq.iq_make_params(d, bits, iq.FULL, SEED, device=0)
+    bad = 0
+    for s in range(25):
+        x = iqsynth.device_unit_vectors(16384, d, 500 + s, TT[dt], "cuda")
+        tn = x.float().norm(dim=1)
+        _, nq = iq.iq_quantize(p, x)
+        _, _, ne = iq.iq_roundtrip(p, x, emit_codes=True)
+        bad += int(((nq - tn).abs() / tn > 1e-5).sum()) + int(((ne - tn).abs() / tn > 1e-5).sum())
+    assert bad == 0
