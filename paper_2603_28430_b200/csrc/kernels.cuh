@@ -153,6 +153,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Warp-wide consumer wait: every lane performs its own acquire of the TMA
+// data (an mbarrier wait by one lane does not make the async-proxy writes
+// visible to the others) in the compiler-visible loop above.  A retry
+// branch inside the asm is treated as warp-uniform by ptxas; since a
+// suspended try_wait can succeed for some lanes and not others, that form let
+// lanes proceed before their acquire and read stale shared memory (observed:
+// ~1e-5 of rows wrong in the first stage of a CTA).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, int) {
+  mbar_wait(bar, parity);
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -531,7 +542,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   int s = 0;
   uint32_t ph = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    mbar_wait(&full[s], ph);
+    mbar_wait_warp(&full[s], ph, lane);
     const uint8_t* st = smem + s * STAGE;
     const int ss_ = s;
     if (++s == NST) { s = 0; ph ^= 1; }
@@ -732,7 +743,7 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
   int s = 0;
   uint32_t ph = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    mbar_wait(&full[s], ph);
+    mbar_wait_warp(&full[s], ph, lane);
     const uint8_t* st = smem + s * STAGE;
     const int64_t v0 = t * TILE_V;
     const int64_t nv = (n - v0) < TILE_V ? (n - v0) : TILE_V;

@@ -17,8 +17,6 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "scaled4": ["-DIQ_SCALED_MAX_BITS=4"],
-    "tpl16": ["-DIQ_TPL=16"],
 }
 
 
