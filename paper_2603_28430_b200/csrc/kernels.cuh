@@ -33,6 +33,9 @@
 namespace iq {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef IQ_RING_KB
+#define IQ_RING_KB 96
+#endif
 #ifndef IQ_PAIR_UNROLL
 #define IQ_PAIR_UNROLL 1
 #endif
@@ -87,15 +90,18 @@ struct Geo {
   static constexpr int NWC = (ENC && SMALL_OPS) ? 16 : 8;         // compute warps per CTA
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
   static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
-  static constexpr int RING = (ENC && SMALL_OPS) ? 200 * 1024 : 96 * 1024;   // TMA ring per CTA
+  static constexpr int RING = (ENC && SMALL_OPS) ? 200 * 1024 : IQ_RING_KB * 1024;   // TMA ring per CTA
   static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
   static constexpr int RB = D * BITS / 8;                          // code bytes per row
   static constexpr int B = EPC * BITS;                             // code bits per chunk
   static constexpr int W = G * B / 32;                             // code words per segment
-  // rows per stage: >= 16 KB of x and a whole number of row pairs per warp
+  // rows per stage: >= STAGE_KB of x and a whole number of row pairs per warp
   // (granule: whole row pairs per warp, and 16-byte aligned norm tiles)
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
-  static constexpr int TV0 = (16384 / ROWB) / GR * GR;
+  // stage size (measured): 32 KB for the b = 3 encoders and the b = 4 fused
+  // kernel (more rows per warp per mbarrier round trip), else 16 KB
+  static constexpr int STAGE_KB = (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32 : 16;
+  static constexpr int TV0 = (STAGE_KB * 1024 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
   static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
@@ -162,6 +168,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // ~1e-5 of rows wrong in the first stage of a CTA).
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, int) {
   mbar_wait(bar, parity);
+}
+
+// Release a ring stage only after the values read from it have been
+// CONSUMED: `dep` is computed from every register the stage's shared-memory
+// loads wrote, and the arrive is predicated on it, so the arrive cannot be
+// issued before those loads have returned their data.  (Arriving right after
+// issuing the loads let the TMA refill of the stage overtake an in-flight
+// load when a warp had only one row pair per stage: rows mixing two tiles'
+// data, observed as ~1e-5 of rows with a wrong norm on a cold first launch.)
+// The predicate must be an INTEGER compare: ptxas folds a float compare
+// against NaN to a constant and drops the dependency.  Lane 0's registers
+// suffice: a warp-wide LDS writes back all lanes together.
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, float dep) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.u32 p, %1, 0x7FC00001;\n"   // always true (a NaN payload no sum produces)
+      "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(bar)),
+      "r"(__float_as_uint(dep))
+      : "memory");
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
@@ -564,10 +589,6 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
         ra[i] = lds128(st + vl * Gm::ROWB + (sub + i * G) * 16);
         rb[i] = lds128(st + (vl + VPW) * Gm::ROWB + (sub + i * G) * 16);
       }
-      if (u + 2 == U) {                                // last rows read: release the stage
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[ss_]);
-      }
       const bool oka = vl < nv, okb = vl + VPW < nv;
       float2 v[EPL];
 #pragma unroll
@@ -576,6 +597,10 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       float2 ss = mul2(v[0], v[0]);
 #pragma unroll
       for (int e = 1; e < EPL; ++e) ss = fma2(v[e], v[e], ss);
+      if (u + 2 == U) {                                // last rows consumed: release the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive_after(&empty[ss_], ss.x + ss.y);
+      }
 #pragma unroll
       for (int o = G / 2; o >= 1; o >>= 1)
         ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
@@ -787,8 +812,17 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
         rho[u] = valid ? ((vl * 4 + 4 <= n16) ? ldsf(st + CODES_B + vl * 4) : __ldg(norms + v0 + vl)) : 0.0f;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    {
+      float dep = 0.0f;                                 // consume every loaded word
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dep += rho[u];
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) dep += __uint_as_float(bits[u][i] & 0x007FFFFFu);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_after(&empty[s], dep);
+    }
     if (++s == NST) { s = 0; ph ^= 1; }
 
 #pragma unroll

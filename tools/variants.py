@@ -4,7 +4,7 @@
   python tools/variants.py time [--d 128 --bits 3 --dtype f16 --variant full]
                                             # on the GPU box: time each variant
 
-Variants differ only in compile-time knobs (-DIQ_TPL, -DIQ_PAIR_UNROLL); the product build is the default one.
+Variants differ only in compile-time knobs (-DIQ_RING_KB, -DIQ_PAIR_UNROLL); the product build is the default one.
 """
 import argparse
 import json
@@ -17,6 +17,7 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
+    "ring160": ["-DIQ_RING_KB=160"],
 }
 
 
