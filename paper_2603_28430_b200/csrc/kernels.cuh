@@ -151,21 +151,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Blocking wait.  The retry loop is C++, NOT a branch inside the asm: a
-// suspended try_wait can release the lanes of a warp at different times, and
-// only a compiler-visible loop lets the compiler reconverge the warp before
-// the shuffles that follow (an asm-internal loop leaves it silently diverged).
+// Blocking wait.  The retry loop is C++ (compiler-visible), so the compiler
+// places the warp's reconvergence point (BSSY/BSYNC) right after it, before
+// the shared loads and shuffles that follow.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
 // Warp-wide consumer wait: every lane performs its own acquire of the TMA
-// data (an mbarrier wait by one lane does not make the async-proxy writes
-// visible to the others) in the compiler-visible loop above.  A retry
-// branch inside the asm is treated as warp-uniform by ptxas; since a
-// suspended try_wait can succeed for some lanes and not others, that form let
-// lanes proceed before their acquire and read stale shared memory (observed:
-// ~1e-5 of rows wrong in the first stage of a CTA).
+// data.  (A rare wrong-row failure first blamed on an asm-internal retry loop
+// was later traced to the stage-release race fixed in mbar_arrive_after.)
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, int) {
   mbar_wait(bar, parity);
 }
