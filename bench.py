@@ -258,7 +258,8 @@ def main():
             dist.all_reduce(t, op=op)
         return t.tolist()
 
-    from paper_2603_28430_b200 import _build
+    from __graft_entry__ import load_builder
+    _build = load_builder()
     if rank == 0:
         _build.build()
     barrier()

@@ -13,7 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def iq():
-    from paper_2603_28430_b200 import _build
+    from __graft_entry__ import load_builder
+    _build = load_builder()
     _build.build()
     import paper_2603_28430_b200 as m
     return m

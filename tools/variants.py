@@ -26,7 +26,8 @@ def lib_path(name):
 
 
 def build(names):
-    from paper_2603_28430_b200 import _build
+    from __graft_entry__ import load_builder
+    _build = load_builder()
     for name in names:
         d = os.path.dirname(lib_path(name))
         _build.build(extra=VARIANTS[name], lib=lib_path(name), objdir=d)
