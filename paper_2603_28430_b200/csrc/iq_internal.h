@@ -24,6 +24,17 @@ struct KCodebook {
   float delta[kMaxHalf];       // delta[m] m>=1: fp32 step with fl(cpos[m-1] + delta[m])
                                // == cpos[m] exactly, so an FMA chain over the
                                // decision indicators lands exactly on C[code]
+  // Uniform-grid decision tables (reading R19).  u = |ybar| * gscale
+  // (gscale a power of two, so u is ybar scaled exactly) falls in cell
+  // j = min(floor(u), NC - 1); each cell holds at most one positive threshold,
+  // so the magnitude code is m_start(j) + [u >= gtab[j]] and, because the
+  // upper part of cell j has the code of the start of cell j + 1, the lookup
+  // index is j + [u >= gtab[j]] into lanes 16..31.
+  float gscale;                // S = 2^k
+  uint32_t gclamp;             // bit pattern of 2^23 + (NC - 1)
+  float gtab[32];              // [j] = nextdown(tau * S) of the threshold in cell j (else +inf);
+                               // [16 + j] = cpos[m_start(j)]
+  uint32_t gcode[32];          // [16 + j] = m_start(j) | h  (code magnitude, sign added later)
 };
 
 // Host-side parameter construction (params.cpp): the reference generator of

@@ -36,6 +36,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_RING_KB
 #define IQ_RING_KB 96
 #endif
+#ifndef IQ_GRID_MIN_BITS
+#define IQ_GRID_MIN_BITS 4   // bits at which the encoders use the grid decision [R19]
+#endif
 #ifndef IQ_PAIR_UNROLL
 #define IQ_PAIR_UNROLL 1
 #endif
@@ -71,6 +74,9 @@ template <class T, int BITS, int KIND>
 constexpr int pick_tpl() {
   constexpr bool f16 = sizeof(T) == 2;
   if (KIND == 3) return 8;
+#ifdef IQ_TPL_K3B4
+  if (KIND == 1 && BITS == 4) return IQ_TPL_K3B4;
+#endif
   if (KIND == 1) return (f16 && BITS == 4) ? 8 : 16;
   return (f16 && BITS <= 3) ? 8 : 16;
 }
@@ -442,6 +448,30 @@ __device__ __forceinline__ void encode_chunk(const float2* y, const RowQ<BITS>& 
   wb = mb ^ (c - sb);
 }
 
+// Uniform-grid decision (reading R19, tables built in params.cpp): u =
+// |ybar| * S with S = 2^k (the caller folds S into the normalisation, so u is
+// exactly the scaled rotated coordinate).  Cell j = min(floor(u), NC - 1)
+// (FADD.RM against 2^23 puts floor(u) in the low mantissa bits), one SHFL
+// fetches the cell's threshold, and the index j + 16 + [u >= threshold]
+// selects the magnitude entry; the shuffles read only the index's low five
+// bits.  Per coordinate: FADD, IMNMX, SHFL, FADD, LEA.HI -- independent of the
+// number of thresholds (7 at b = 4).
+__device__ __forceinline__ uint32_t grid_index(float y, float gtab, uint32_t gclamp) {
+  const float au = fabsf(y);
+  uint32_t t = __float_as_uint(__fadd_rd(au, 8388608.0f));
+  t = min(t, gclamp);
+  // the table holds nextdown(threshold): u >= threshold <=> nextdown - u < 0,
+  // and the sign bit of that difference is the increment (ties go up [R3])
+  const float dlt = __shfl_sync(kFull, gtab, (int)t) - au;
+  return t + 16u + (__float_as_uint(dlt) >> 31);
+}
+// signed code of a grid index: (m | h) for ybar >= 0, h - 1 - m = (m | h) ^ (2h - 1) below
+template <int BITS>
+__device__ __forceinline__ uint32_t grid_code(uint32_t idx, float y, uint32_t gcode) {
+  const uint32_t mh = (uint32_t)__shfl_sync(kFull, (int)gcode, (int)idx);
+  return mh ^ ((uint32_t)((int)__float_as_uint(y) >> 31) & ((1u << BITS) - 1u));
+}
+
 // ------------------------------------------------------------- bit packing
 // A lane's chunk contributes B = EPC*BITS consecutive bits of the row's
 // LSB-first bitstream [R7].  G lanes form a segment of G*B bits = W words.
@@ -558,6 +588,9 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   constexpr bool emit = MODE != 1;
   constexpr bool value = MODE != 0;
   const float ctab = cb.cent[lane & ((1 << BITS) - 1)];   // C[k] in lane k of each group of L
+  constexpr bool GRID = BITS >= IQ_GRID_MIN_BITS;          // uniform-grid decision [R19]
+  const float gtab = cb.gtab[lane];
+  const uint32_t gcode = cb.gcode[lane];
 
   int s = 0;
   uint32_t ph = 0;
@@ -600,6 +633,41 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       for (int o = G / 2; o >= 1; o >>= 1)
         ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
       const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
+      float2 out[EPL];
+      uint32_t cwa[CPL], cwb[CPL];
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
+      if constexpr (GRID) {
+        // ybar * S = T(x * S / max(rho, eps)): one exact power-of-two scaling
+        // folded into the normalisation (Alg.1 l.1) [R19]
+        const float2 sc = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)) * cb.gscale,
+                             rsqrt_ftz(fmaxf(ss.y, 1e-24f)) * cb.gscale);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) v[e] = mul2(v[e], sc);
+#pragma unroll
+        for (int b = 0; b < NBL; ++b) {
+          float2 yb[PW], cq[PW];
+          rot_fwd<PW>(P[b], v + b * PW, yb);             // S * T(xbar)  (Alg.1 l.5/9/13)
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            const uint32_t ia = grid_index(yb[j].x, gtab, cb.gclamp);
+            const uint32_t ib = grid_index(yb[j].y, gtab, cb.gclamp);
+            if constexpr (emit) {
+              const int e = (b * PW + j) % EPC, c = (b * PW + j) / EPC;
+              cwa[c] |= grid_code<BITS>(ia, yb[j].x, gcode) << (e * BITS);
+              cwb[c] |= grid_code<BITS>(ib, yb[j].y, gcode) << (e * BITS);
+            }
+            if constexpr (value)                         // v^ = C[code] (sign restored)
+              cq[j] = f2(sign_xor(__shfl_sync(kFull, gtab, (int)ia), yb[j].x),
+                         sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[j].y));
+          }
+          if constexpr (value) {
+            rot_inv<PW>(P[b], cq, out + b * PW);         // T^-1 (l.7/11/15)
+#pragma unroll
+            for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);   // x^ = rho * ...
+          }
+        }
+      } else {
       // Decision rule (R14c).  SCALED: compare y = T(x) with per-row
       // thresholds r*tau, r = max(rho, eps) (saves normalising the row).
       // K1 (MODE 0) and K3+codes (MODE 2) always use it, so they emit
@@ -618,10 +686,6 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
         inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
       }
 
-      float2 out[EPL];
-      uint32_t cwa[CPL], cwb[CPL];
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
       if constexpr (!emit) {                             // K3: values only
 #pragma unroll
         for (int b = 0; b < NBL; ++b) {
@@ -671,6 +735,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
           }
         }
       }
+      }  // !GRID
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         if constexpr (value) {

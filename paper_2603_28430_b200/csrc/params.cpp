@@ -120,6 +120,68 @@ std::vector<double> lloyd_max_gaussian(int bits) {
   return out;
 }
 
+// Uniform-grid decision tables (reading R19, see KCodebook).  S is the
+// largest power of two for which the last positive threshold lands in a cell
+// below 15 (so NC = cell + 2 <= 16); the cells of the thresholds must then be
+// distinct.  The construction is verified exhaustively against the counting
+// definition code = #{m : u >= tau_m S} on every threshold, its fp32
+// neighbours and every cell boundary.
+bool build_grid(KCodebook& kc, int h, std::string* err) {
+  const float inf = std::numeric_limits<float>::infinity();
+  const float tmax = h > 1 ? kc.tau[h - 1] : 0.0f;
+  float S = 1.0f;
+  if (h > 1) {
+    S = std::ldexp(1.0f, 40);
+    while (S > 0.0f && std::floor(tmax * S) > 14.0f) S *= 0.5f;
+  }
+  int cell[kMaxHalf] = {0};
+  for (int m = 1; m < h; ++m) {
+    cell[m] = static_cast<int>(std::floor(kc.tau[m] * S));   // tau * S exact (S = 2^k)
+    if (m > 1 && cell[m] <= cell[m - 1]) { *err = "grid: two thresholds share a cell"; return false; }
+  }
+  const int nc = (h > 1 ? cell[h - 1] : -1) + 2;
+  if (nc > 16) { *err = "grid: more than 16 cells"; return false; }
+  kc.gscale = S;
+  kc.gclamp = 0x4B000000u + static_cast<uint32_t>(nc - 1);
+  for (int j = 0; j < 16; ++j) {
+    float t = inf;
+    int mstart = 0;
+    for (int m = 1; m < h; ++m) {
+      if (cell[m] == j) t = std::nextafter(kc.tau[m] * S, 0.0f);   // nextdown (see grid_index)
+      if (cell[m] < j) ++mstart;
+    }
+    kc.gtab[j] = t;
+    kc.gtab[16 + j] = kc.cpos[mstart];
+    kc.gcode[j] = 0u;
+    kc.gcode[16 + j] = static_cast<uint32_t>(mstart | h);
+  }
+  // check the decision at every threshold, its fp32 neighbours and every
+  // cell boundary against the counting definition
+  std::vector<float> probes = {0.0f, 1e30f};   // (the kernels' u is finite)
+  for (int m = 1; m < h; ++m) {
+    const float t = kc.tau[m] * S;
+    probes.insert(probes.end(), {t, std::nextafter(t, 0.0f), std::nextafter(t, inf)});
+  }
+  for (int j = 0; j <= 17; ++j) {
+    const float b = static_cast<float>(j);
+    probes.insert(probes.end(), {b, std::nextafter(b, 0.0f), std::nextafter(b, inf)});
+  }
+  for (float u : probes) {
+    int want = 0;
+    for (int m = 1; m < h; ++m) want += (u >= kc.tau[m] * S);
+    float fl = std::floor(u);
+    uint32_t j = fl >= static_cast<float>(nc - 1) ? static_cast<uint32_t>(nc - 1) : static_cast<uint32_t>(fl);
+    const float dlt = kc.gtab[j] - u;                            // the kernel's test
+    const uint32_t idx = (j + (std::signbit(dlt) ? 1u : 0u)) & 15u;
+    const int got = static_cast<int>(kc.gcode[16 + idx]) - h;
+    if (got != want || kc.gtab[16 + idx] != kc.cpos[want]) {
+      *err = "grid: decision table self-check failed";
+      return false;
+    }
+  }
+  return true;
+}
+
 }  // namespace
 
 size_t rotation_param_count(int d, int variant) {
@@ -220,6 +282,7 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
     if (probe != b) { *err = "no exact fp32 codebook step"; return false; }
     kc.delta[m] = dlt;
   }
+  if (!build_grid(kc, h, err)) return false;
   return true;
 }
 

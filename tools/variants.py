@@ -17,7 +17,10 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "ring160": ["-DIQ_RING_KB=160"],
+    "nogrid": ["-DIQ_GRID_MIN_BITS=5"],
+    "tpl16": ["-DIQ_TPL_K3B4=16"],
+    "grid3": ["-DIQ_GRID_MIN_BITS=3"],
+    "grid3tpl16": ["-DIQ_GRID_MIN_BITS=3", "-DIQ_TPL_K3B4=16"],
 }
 
 
