@@ -39,6 +39,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_GRID_MIN_BITS
 #define IQ_GRID_MIN_BITS 4   // bits at which the encoders use the grid decision [R19]
 #endif
+#ifndef IQ_OPS_SMEM
+#define IQ_OPS_SMEM 1        // large-operator encoders read their operators from shared memory
+#endif
 #ifndef IQ_PAIR_UNROLL
 #define IQ_PAIR_UNROLL 1
 #endif
@@ -67,9 +70,9 @@ constexpr int pick_cpl() {
 
 // Kernel kinds: 0 quantize (K1), 1 fused roundtrip (K3), 2 fused roundtrip +
 // codes, 3 dequantize (K2).  Coordinates per lane (TPL), measured on B200
-// (DESIGN.md section 6): K3 16 except fp16 b = 4 (8); K1 and K3+codes share
-// one geometry so that they emit bit-identical codes and norms: 8 for fp16
-// b <= 3, else 16; the decoder 8.
+// (DESIGN.md section 6): 16 for every encoder except the fp32 code-emitting
+// ones (8); K1 and K3+codes share one geometry so that they emit
+// bit-identical codes and norms; the decoder 8.
 template <class T, int BITS, int KIND>
 constexpr int pick_tpl() {
   constexpr bool f16 = sizeof(T) == 2;
@@ -77,8 +80,20 @@ constexpr int pick_tpl() {
 #ifdef IQ_TPL_K3B4
   if (KIND == 1 && BITS == 4) return IQ_TPL_K3B4;
 #endif
-  if (KIND == 1) return (f16 && BITS == 4) ? 8 : 16;
-  return (f16 && BITS <= 3) ? 8 : 16;
+  if (KIND == 1) return 16;
+#ifdef IQ_TPL_EMIT
+  return IQ_TPL_EMIT;
+#endif
+  return f16 ? 16 : 8;
+}
+// Where an encoder whose operators exceed 32 registers per lane keeps them
+// (measured): shared memory (16 compute warps) for fp16 except the b <= 2
+// fused kernel, and for the fp32 quantizer; registers (8 warps) otherwise.
+template <class T, int BITS, int KIND>
+constexpr bool pick_ops_smem() {
+  if (!IQ_OPS_SMEM || KIND == 3) return false;
+  if (sizeof(T) == 2) return !(KIND == 1 && BITS <= 2);
+  return KIND == 0;
 }
 
 template <class T, int D, int BITS, int VAR, int KIND>
@@ -93,10 +108,16 @@ struct Geo {
   static constexpr int EPL = CPL * EPC;                            // coordinates per lane
   static constexpr int NBL = EPL / PW;                             // blocks per lane
   static constexpr bool SMALL_OPS = NBL * PW * PW <= 32;
-  static constexpr int NWC = (ENC && SMALL_OPS) ? 16 : 8;         // compute warps per CTA
+  // encoders whose operators do not fit 32 registers per lane keep them in
+  // shared memory (lane-contiguous float4 columns, re-read per block) so that
+  // 16 compute warps fit the register file
+  static constexpr bool OPS_SMEM = ENC && !SMALL_OPS && pick_ops_smem<T, BITS, KIND>();
+  static constexpr bool WIDE = ENC && (SMALL_OPS || OPS_SMEM);
+  static constexpr int NWC = WIDE ? 16 : 8;                        // compute warps per CTA
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
   static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
-  static constexpr int RING = (ENC && SMALL_OPS) ? 200 * 1024 : IQ_RING_KB * 1024;   // TMA ring per CTA
+  static constexpr int OPS_BYTES = OPS_SMEM ? G * NBL * PW * PW * 4 : 0;
+  static constexpr int RING = WIDE ? 200 * 1024 - OPS_BYTES : IQ_RING_KB * 1024;   // TMA ring per CTA
   static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
   static constexpr int RB = D * BITS / 8;                          // code bytes per row
   static constexpr int B = EPC * BITS;                             // code bits per chunk
@@ -112,6 +133,8 @@ struct Geo {
   static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
   static constexpr int ENC_STAGES = (RING / ENC_STAGE) < 12 ? (RING / ENC_STAGE) : 12;
+  static constexpr int OPS_OFF = (ENC_STAGES * ENC_STAGE + 2 * ENC_STAGES * 8 + 64 + 127) / 128 * 128;
+  static constexpr int ENC_SMEM = OPS_OFF + OPS_BYTES;             // dynamic shared memory
   // decoder stage: codes tile (16-B aligned) followed by the norms tile
   static constexpr int DEC_CODES = (TILE_V * RB + 15) / 16 * 16;
   static constexpr int DEC_STAGE = (DEC_CODES + TILE_V * 4 + 127) / 128 * 128;
@@ -525,6 +548,40 @@ __device__ __forceinline__ void load_ops(const float* __restrict__ mat, int sub,
   }
 }
 
+// Operators in shared memory: float4 q of block b of lane `sub` lives at
+// float4 index (b * NQ + q) * G + sub, so the G lanes of a row read 16 G
+// contiguous bytes (the VPW row groups of a warp read the same addresses:
+// broadcast, no bank conflicts).  Written once per CTA by compute warp 0.
+template <class Gm>
+__device__ __forceinline__ void store_ops_smem(uint8_t* ops, int sub, const float (&P)[Gm::NBL][Gm::PW * Gm::PW]) {
+  constexpr int NQ = Gm::PW * Gm::PW / 4;
+#pragma unroll
+  for (int b = 0; b < Gm::NBL; ++b)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      reinterpret_cast<float4*>(ops)[(b * NQ + q) * Gm::G + sub] =
+          make_float4(P[b][4 * q], P[b][4 * q + 1], P[b][4 * q + 2], P[b][4 * q + 3]);
+}
+// The operator of block b: the register copy, or (OPS_SMEM) a volatile
+// shared-memory read right before use, which keeps it out of the loop-
+// invariant register set.
+template <class Gm>
+__device__ __forceinline__ void fetch_op(const float (&P)[Gm::OPS_SMEM ? 1 : Gm::NBL][Gm::PW * Gm::PW],
+                                         const uint8_t* ops, int sub, int b, float (&M)[Gm::PW * Gm::PW]) {
+  constexpr int NQ = Gm::PW * Gm::PW / 4;
+  if constexpr (Gm::OPS_SMEM) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint4 t = lds128(ops + 16 * ((b * NQ + q) * Gm::G + sub));
+      M[4 * q] = __uint_as_float(t.x); M[4 * q + 1] = __uint_as_float(t.y);
+      M[4 * q + 2] = __uint_as_float(t.z); M[4 * q + 3] = __uint_as_float(t.w);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Gm::PW * Gm::PW; ++k) M[k] = P[b][k];
+  }
+}
+
 // Ring setup shared by the three kernels.
 template <int NST, int NWC>
 __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
@@ -583,8 +640,18 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   const int sub = lane & (G - 1);
   const int vbase = lane & ~(G - 1);
   const int vslot = lane / G;
-  float P[NBL][PW * PW];
-  load_ops<Gm>(mat, sub, P);
+  float P[Gm::OPS_SMEM ? 1 : NBL][PW * PW];
+  uint8_t* const ops = smem + Gm::OPS_OFF;
+  if constexpr (Gm::OPS_SMEM) {
+    if (warp == 0 && lane < G) {
+      float Pl[NBL][PW * PW];
+      load_ops<Gm>(mat, sub, Pl);
+      store_ops_smem<Gm>(ops, sub, Pl);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // compute warps only
+  } else {
+    load_ops<Gm>(mat, sub, P);
+  }
   constexpr bool emit = MODE != 1;
   constexpr bool value = MODE != 0;
   const float ctab = cb.cent[lane & ((1 << BITS) - 1)];   // C[k] in lane k of each group of L
@@ -647,7 +714,9 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
         for (int b = 0; b < NBL; ++b) {
           float2 yb[PW], cq[PW];
-          rot_fwd<PW>(P[b], v + b * PW, yb);             // S * T(xbar)  (Alg.1 l.5/9/13)
+          float Mb[PW * PW];
+          fetch_op<Gm>(P, ops, sub, b, Mb);
+          rot_fwd<PW>(Mb, v + b * PW, yb);               // S * T(xbar)  (Alg.1 l.5/9/13)
 #pragma unroll
           for (int j = 0; j < PW; ++j) {
             const uint32_t ia = grid_index(yb[j].x, gtab, cb.gclamp);
@@ -662,7 +731,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
                          sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[j].y));
           }
           if constexpr (value) {
-            rot_inv<PW>(P[b], cq, out + b * PW);         // T^-1 (l.7/11/15)
+            rot_inv<PW>(Mb, cq, out + b * PW);           // T^-1 (l.7/11/15)
 #pragma unroll
             for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);   // x^ = rho * ...
           }
@@ -690,13 +759,15 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
         for (int b = 0; b < NBL; ++b) {
           float2 yb[PW], cq[PW];
+          float Mb[PW * PW];
+          fetch_op<Gm>(P, ops, sub, b, Mb);
           if constexpr (SCALED) {
-            rot_fwd<PW>(P[b], v + b * PW, yb);           // y = T(x)  (Alg.1 l.5/9/13, [R14c])
+            rot_fwd<PW>(Mb, v + b * PW, yb);           // y = T(x)  (Alg.1 l.5/9/13, [R14c])
           } else {
             float2 xb[PW];
 #pragma unroll
             for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
-            rot_fwd<PW>(P[b], xb, yb);                   // v~ = T(xbar)
+            rot_fwd<PW>(Mb, xb, yb);                     // v~ = T(xbar)
           }
 #pragma unroll
           for (int j = 0; j < PW; ++j) {
@@ -704,7 +775,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
             if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
             else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
           }
-          rot_inv<PW>(P[b], cq, out + b * PW);           // x^ = T^-1(rho * v^)  (l.7/11/15)
+          rot_inv<PW>(Mb, cq, out + b * PW);             // x^ = T^-1(rho * v^)  (l.7/11/15)
           if constexpr (RESCALE) {
 #pragma unroll
             for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
@@ -715,9 +786,12 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           float2 yb[EPC];
+          float Mc[BPCH][PW * PW];
 #pragma unroll
-          for (int bb = 0; bb < BPCH; ++bb)
-            rot_fwd<PW>(P[i * BPCH + bb], v + i * EPC + bb * PW, yb + bb * PW);   // y = T(x)
+          for (int bb = 0; bb < BPCH; ++bb) {
+            fetch_op<Gm>(P, ops, sub, i * BPCH + bb, Mc[bb]);
+            rot_fwd<PW>(Mc[bb], v + i * EPC + bb * PW, yb + bb * PW);             // y = T(x)
+          }
           encode_chunk<BITS, EPC>(yb, q, cwa[i], cwb[i]);                       // codes of Q(y)
           if constexpr (value) {
             float2 cq[EPC];
@@ -728,7 +802,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
             for (int bb = 0; bb < BPCH; ++bb) {
               float2* o = out + i * EPC + bb * PW;
-              rot_inv<PW>(P[i * BPCH + bb], cq + bb * PW, o);   // T^-1
+              rot_inv<PW>(Mc[bb], cq + bb * PW, o);             // T^-1
 #pragma unroll
               for (int j = 0; j < PW; ++j) o[j] = mul2(o[j], rho);   // x^ = rho * ...
             }

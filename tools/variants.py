@@ -17,10 +17,10 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "nogrid": ["-DIQ_GRID_MIN_BITS=5"],
+    "opsreg": ["-DIQ_OPS_SMEM=0"],
     "tpl16": ["-DIQ_TPL_K3B4=16"],
-    "grid3": ["-DIQ_GRID_MIN_BITS=3"],
-    "grid3tpl16": ["-DIQ_GRID_MIN_BITS=3", "-DIQ_TPL_K3B4=16"],
+    "emit16": ["-DIQ_TPL_EMIT=16"],
+    "emit8": ["-DIQ_TPL_EMIT=8"],
 }
 
 
