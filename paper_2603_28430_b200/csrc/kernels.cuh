@@ -42,6 +42,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_OPS_SMEM
 #define IQ_OPS_SMEM 1        // large-operator encoders read their operators from shared memory
 #endif
+#ifndef IQ_NWC_WIDE
+#define IQ_NWC_WIDE 16       // compute warps of the wide encoder CTAs
+#endif
+#ifndef IQ_B3_ALU
+#define IQ_B3_ALU 1          // b = 3 fused value chain: FSETP + predicated FADD (else FSET + FFMA2)
+#endif
 #ifndef IQ_PAIR_UNROLL
 #define IQ_PAIR_UNROLL 1
 #endif
@@ -80,6 +86,9 @@ constexpr int pick_tpl() {
 #ifdef IQ_TPL_K3B4
   if (KIND == 1 && BITS == 4) return IQ_TPL_K3B4;
 #endif
+#ifdef IQ_TPL_K3
+  if (KIND == 1) return IQ_TPL_K3;
+#endif
   if (KIND == 1) return 16;
 #ifdef IQ_TPL_EMIT
   return IQ_TPL_EMIT;
@@ -113,7 +122,7 @@ struct Geo {
   // 16 compute warps fit the register file
   static constexpr bool OPS_SMEM = ENC && !SMALL_OPS && pick_ops_smem<T, BITS, KIND>();
   static constexpr bool WIDE = ENC && (SMALL_OPS || OPS_SMEM);
-  static constexpr int NWC = WIDE ? 16 : 8;                        // compute warps per CTA
+  static constexpr int NWC = WIDE ? IQ_NWC_WIDE : 8;               // compute warps per CTA
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
   static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
   static constexpr int OPS_BYTES = OPS_SMEM ? G * NBL * PW * PW * 4 : 0;
@@ -127,12 +136,16 @@ struct Geo {
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
   // stage size (measured): 32 KB for the b = 3 encoders and the b = 4 fused
   // kernel (more rows per warp per mbarrier round trip), else 16 KB
+#ifdef IQ_STAGE_KB
+  static constexpr int STAGE_KB = ENC ? IQ_STAGE_KB : 16;
+#else
   static constexpr int STAGE_KB = (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32 : 16;
+#endif
   static constexpr int TV0 = (STAGE_KB * 1024 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
   static constexpr int U = TILE_V / (NWC * VPW);                  // rows per lane group per stage
   static constexpr int ENC_STAGE = TILE_V * ROWB;
-  static constexpr int ENC_STAGES = (RING / ENC_STAGE) < 12 ? (RING / ENC_STAGE) : 12;
+  static constexpr int ENC_STAGES = (RING / ENC_STAGE) < 2 ? 2 : (RING / ENC_STAGE) < 12 ? (RING / ENC_STAGE) : 12;
   static constexpr int OPS_OFF = (ENC_STAGES * ENC_STAGE + 2 * ENC_STAGES * 8 + 64 + 127) / 128 * 128;
   static constexpr int ENC_SMEM = OPS_OFF + OPS_BYTES;             // dynamic shared memory
   // decoder stage: codes tile (16-B aligned) followed by the norms tile
@@ -384,7 +397,7 @@ __device__ __forceinline__ float2 quantize_pair(float2 y, const RowQ<BITS>& q, u
   float2 m = bc(8388608.0f);  // 2^23
 #pragma unroll
   for (int i = 1; i < H; ++i) {
-    if constexpr (VALUE && !CODE && BITS == 3) {
+    if constexpr (VALUE && !CODE && BITS == 3 && IQ_B3_ALU) {
       // b = 3: conditional add on the ALU (FSETP + predicated FADD) instead of
       // the indicator FFMA2 -- shifts work off the FMA pipe (+3% measured)
       c.x = ka >= q.thr[i].x ? c.x + q.dl[i].x : c.x;

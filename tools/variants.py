@@ -17,10 +17,10 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "opsreg": ["-DIQ_OPS_SMEM=0"],
-    "tpl16": ["-DIQ_TPL_K3B4=16"],
-    "emit16": ["-DIQ_TPL_EMIT=16"],
-    "emit8": ["-DIQ_TPL_EMIT=8"],
+    "opsreg": ["-DIQ_OPS_SMEM=0"],          # operators always in registers (8-warp CTAs)
+    "nwc12": ["-DIQ_NWC_WIDE=12"],          # 12 compute warps in the wide encoder CTAs
+    "b3fma": ["-DIQ_B3_ALU=0"],             # b = 3 chain as FSET + FFMA2
+    "stage64": ["-DIQ_STAGE_KB=64"],        # 64 KB ring stages
 }
 
 
