@@ -177,6 +177,49 @@ iq_status iq_dequantize(const iq_params* p, int dtype, int64_t n,
 iq_status iq_roundtrip(const iq_params* p, int dtype, int64_t n, const void* x,
                        void* y, uint8_t* codes, float* norms, void* cuda_stream);
 
+/* ------------------------------------------------------------------------
+ * Stage 2: residual sketch (QJL-style correction, PAPER.md section
+ * "Compatibility with Residual Correction"; R20-R24).
+ * The paper fixes only r = x - x^_mse and "project the residual with a
+ * quantized Johnson-Lindenstrauss transform"; the rest is our reading:
+ *  - S is m x d with m = d, S[i][k] = fp16_rn(N_(i*d+k)), N_j the j-th
+ *    standard normal of the [R12] generator keyed with seed ^
+ *    0x514A4C534B455443.  The fp16-rounded values are the sketch.
+ *  - r = x - x^ with x^ = rho T^-1(C[code]) evaluated in fp32 (before any
+ *    rounding to dtype); gamma = ||r||_2 (fp32).
+ *  - q_i = +1 if (S r)_i >= 0 else -1; stored LSB-first, bit i of a row set
+ *    iff q_i = +1.  Rows of qjl are iq_qjl_bytes_per_vector(d) = d/8 bytes.
+ *  - Estimators a consumer builds from (codes, norms, qjl, rnorms):
+ *      <y, x> ~= <y, x^> + sqrt(pi/2)/m * gamma * <S y, q>,
+ *      x~ = x^ + sqrt(pi/2)/m * gamma * S^T q  (unbiased over S).
+ * ------------------------------------------------------------------------ */
+
+/* iq_make_params plus the stage-2 sketch S (m = d).  The GPU sketch kernel
+ * supports d in {64, 128} (UNSUPPORTED otherwise when device >= 0). */
+iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int device,
+                             iq_params** out);
+
+/* Sketch bytes per row: ceil(m / 8) with m = d. */
+size_t iq_qjl_bytes_per_vector(int d);
+
+/* Copy S (row-major [m][d], the fp16 values widened to float) to a host
+ * buffer of len >= m*d floats.  INVALID_ARGUMENT if the handle has no
+ * sketch, BUFFER_TOO_SMALL if len is short. */
+iq_status iq_export_qjl_matrix(const iq_params* p, float* S, size_t len);
+
+/*
+ * iq_quantize_qjl — stage 1 + stage 2 in one kernel: x[n,d] -> codes, norms
+ * (bit-identical to iq_quantize), qjl[n, d/8] sign bits of S r and
+ * rnorms[n] = ||r||.  One persistent kernel: TMA ring for x, the stage-1
+ * encoder in CUDA cores, r split into fp16 hi + lo tiles in shared memory,
+ * z = S (r_hi + r_lo) on the tensor cores (tcgen05.mma, fp32 accumulators in
+ * TMEM), sign packing from TMEM.  x 16-byte aligned; codes, norms, rnorms
+ * 4-byte and qjl 8-byte aligned.
+ */
+iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* x,
+                          uint8_t* codes, float* norms, uint8_t* qjl, float* rnorms,
+                          void* cuda_stream);
+
 /*
  * iq_error_sums — reconstruction statistics on the device (not part of the
  * timed path): sums[0] += sum_{i,j} (x_ij - y_ij)^2, sums[1] += sum x_ij^2,

@@ -22,6 +22,7 @@ __all__ = [
     "iq_make_params", "iq_quantize", "iq_dequantize", "iq_roundtrip", "iq_error_sums",
     "iq_export_params", "iq_export_block_matrices", "iq_code_bytes_per_vector",
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
+    "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -56,6 +57,10 @@ _sig = {
     "iq_host_pipeline_create": (_c_int, [_c_vp, _c_int, _c_i64, ctypes.POINTER(_c_vp)]),
     "iq_host_pipeline_destroy": (_c_int, [_c_vp]),
     "iq_host_roundtrip": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_make_params_qjl": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, ctypes.POINTER(_c_vp)]),
+    "iq_qjl_bytes_per_vector": (_c_sz, [_c_int]),
+    "iq_export_qjl_matrix": (_c_int, [_c_vp, _c_vp, _c_sz]),
+    "iq_quantize_qjl": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -124,6 +129,27 @@ def iq_make_params(d: int, bits: int, variant, seed: int, device: int = 0) -> Pa
     _check(lib.iq_make_params(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
                               int(device), ctypes.byref(h)), "iq_make_params")
     return Params(h.value, d, bits, variant, seed, device)
+
+
+def iq_make_params_qjl(d: int, bits: int, variant, seed: int, device: int = 0) -> Params:
+    """iq_make_params plus the stage-2 residual sketch S (m = d)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant.lower()]
+    h = ctypes.c_void_p()
+    _check(lib.iq_make_params_qjl(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
+                                  int(device), ctypes.byref(h)), "iq_make_params_qjl")
+    return Params(h.value, d, bits, variant, seed, device)
+
+
+def iq_qjl_bytes_per_vector(d: int) -> int:
+    return int(lib.iq_qjl_bytes_per_vector(d))
+
+
+def iq_export_qjl_matrix(p: Params) -> np.ndarray:
+    """S [m, d] (fp16 values as float32)."""
+    S = np.zeros((p.d, p.d), dtype=np.float32)
+    _check(lib.iq_export_qjl_matrix(p.handle, S.ctypes.data, S.size), "iq_export_qjl_matrix")
+    return S
 
 
 def iq_export_params(p: Params) -> dict:
@@ -213,6 +239,24 @@ def iq_roundtrip(p: Params, x, y=None, codes=None, norms=None, emit_codes: bool 
     _check(lib.iq_roundtrip(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(codes), _ptr(norms),
                             _stream_ptr(stream)), "iq_roundtrip")
     return (y, codes, norms) if codes is not None else y
+
+
+def iq_quantize_qjl(p: Params, x, codes=None, norms=None, qjl=None, rnorms=None, stream=None):
+    """x [n,d] -> (codes, norms, qjl [n, d/8] uint8, rnorms [n] f32): stage 1 +
+    stage-2 residual sketch in one kernel."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    if codes is None:
+        codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
+    if norms is None:
+        norms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    if qjl is None:
+        qjl = torch.empty((n, iq_qjl_bytes_per_vector(p.d)), dtype=torch.uint8, device=x.device)
+    if rnorms is None:
+        rnorms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    _check(lib.iq_quantize_qjl(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms), _ptr(qjl),
+                               _ptr(rnorms), _stream_ptr(stream)), "iq_quantize_qjl")
+    return codes, norms, qjl, rnorms
 
 
 def iq_error_sums(p: Params, x, y, sums=None, stream=None):

@@ -1,6 +1,7 @@
 // C ABI of libisoquant (include/isoquant.h): validation, parameter handles,
 // dispatch to the template instances, reconstruction statistics and the
 // host-buffer streaming pipeline.  No exception crosses this boundary.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,6 +39,7 @@ struct iq_params {
   iq::HostParams hp;
   int device = -1;
   float* d_mat = nullptr;
+  uint8_t* d_qjl = nullptr;   // UMMA image of the stage-2 sketch S (iq_make_params_qjl)
 };
 
 namespace {
@@ -116,17 +118,22 @@ const char* iq_status_string(iq_status s) {
 
 const char* iq_last_error_detail(void) { return g_detail.c_str(); }
 
-iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device,
-                         iq_params** out) {
+static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, int device, bool qjl,
+                                  iq_params** out) {
   if (!out) return fail(IQ_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (device < -1) return fail(IQ_ERR_INVALID_ARGUMENT, "device must be >= -1");
   iq_params* p = new (std::nothrow) iq_params();
   if (!p) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
   std::string err;
-  if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err)) {
+  if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err) ||
+      (qjl && !iq::build_qjl(&p->hp, &err))) {
     delete p;
     return fail(IQ_ERR_INVALID_ARGUMENT, err);
+  }
+  if (qjl && device >= 0 && !iq::qjl_supported(d)) {
+    delete p;
+    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 sketch kernel supports d in {64, 128}");
   }
   p->device = device;
   if (device >= 0) {
@@ -141,15 +148,27 @@ iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_mat, p->hp.mat.data(), p->hp.mat.size() * sizeof(float),
                      cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl, p->hp.qjl_img.size());
+    if (e == cudaSuccess && qjl)
+      e = cudaMemcpy(p->d_qjl, p->hp.qjl_img.data(), p->hp.qjl_img.size(), cudaMemcpyHostToDevice);
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
     if (e != cudaSuccess) {
       if (p->d_mat) cudaFree(p->d_mat);
+      if (p->d_qjl) cudaFree(p->d_qjl);
       delete p;
       return cuda_fail(e, "iq_make_params device upload");
     }
   }
   *out = p;
   return IQ_OK;
+}
+
+iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device, iq_params** out) {
+  return make_params_impl(d, bits, variant, seed, device, false, out);
+}
+
+iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int device, iq_params** out) {
+  return make_params_impl(d, bits, variant, seed, device, true, out);
 }
 
 iq_status iq_free_params(iq_params* p) {
@@ -159,6 +178,7 @@ iq_status iq_free_params(iq_params* p) {
     cudaGetDevice(&prev);
     if (prev != p->device) cudaSetDevice(p->device);
     cudaFree(p->d_mat);
+    if (p->d_qjl) cudaFree(p->d_qjl);
     if (prev >= 0 && prev != p->device) cudaSetDevice(prev);
   }
   delete p;
@@ -210,6 +230,46 @@ iq_status iq_export_block_matrices(const iq_params* p, float* m, size_t m_len) {
   if (m_len < p->hp.mat.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "matrix buffer too small");
   std::memcpy(m, p->hp.mat.data(), p->hp.mat.size() * sizeof(float));
   return IQ_OK;
+}
+
+size_t iq_qjl_bytes_per_vector(int d) {
+  if (d <= 0) return 0;
+  return (static_cast<size_t>(d) + 7) / 8;
+}
+
+iq_status iq_export_qjl_matrix(const iq_params* p, float* S, size_t len) {
+  if (!p || !S) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!p->hp.has_qjl) return fail(IQ_ERR_INVALID_ARGUMENT, "handle has no stage-2 sketch (use iq_make_params_qjl)");
+  const size_t need = p->hp.qjl_half.size();
+  if (len < need) return fail(IQ_ERR_BUFFER_TOO_SMALL, "S buffer too small (m * d floats)");
+  for (size_t i = 0; i < need; ++i) {
+    __half_raw r;
+    r.x = p->hp.qjl_half[i];
+    S[i] = __half2float(__half(r));
+  }
+  return IQ_OK;
+}
+
+iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* x, uint8_t* codes,
+                          float* norms, uint8_t* qjl, float* rnorms, void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (!p->hp.has_qjl || !p->d_qjl)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "handle has no stage-2 sketch (use iq_make_params_qjl)");
+  if (n == 0) return IQ_OK;
+  if (!x || !codes || !norms || !qjl || !rnorms)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "x, codes, norms, qjl and rnorms are required");
+  if (!aligned(x, 16)) return fail(IQ_ERR_MISALIGNED, "x must be 16-byte aligned");
+  if (!aligned(codes, 4) || !aligned(norms, 4) || !aligned(rnorms, 4) || !aligned(qjl, 8))
+    return fail(IQ_ERR_MISALIGNED, "codes, norms, rnorms must be 4-byte and qjl 8-byte aligned");
+  iq::LaunchArgs a = base_args(p, n, stream);
+  a.x = x;
+  a.codes = codes;
+  a.norms = norms;
+  a.qjl_img = p->d_qjl;
+  a.qjl = qjl;
+  a.rnorms = rnorms;
+  return run(iq::Kernel::kQuantizeQjl, p, dtype, a);
 }
 
 iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x, uint8_t* codes,

@@ -47,7 +47,28 @@ struct HostParams {
   std::vector<float> centroids;   // [L] fp32 ascending
   std::vector<float> thresholds;  // [L-1] fp32 ascending
   KCodebook kcb{};
+  // Stage-2 residual sketch (R20): S [m = d][d] of fp16-rounded
+  // N(0,1) draws, row-major half bits, and the UMMA operand image (K-major,
+  // 128-byte swizzle) the sketch kernel copies into shared memory.
+  bool has_qjl = false;
+  std::vector<uint16_t> qjl_half;
+  std::vector<uint8_t> qjl_img;
 };
+
+// Sketch generator key and layout (params.cpp).
+bool build_qjl(HostParams* hp, std::string* err);
+bool qjl_supported(int d);   // GPU sketch kernel: d in {64, 128}
+// byte offset of element (row r, k) in a K-major 128B-swizzled UMMA operand
+// with `rows` rows: K slabs of 64 fp16, 8-row atoms of 1024 B
+#ifdef __CUDACC__
+#define IQ_HD __host__ __device__
+#else
+#define IQ_HD
+#endif
+IQ_HD inline uint32_t umma_sw128_off(int r, int k, int rows) {
+  return static_cast<uint32_t>((k / 64) * (rows / 8) * 1024 + (r / 8) * 1024 + (r % 8) * 128 +
+                               ((((k % 64) / 8) ^ (r % 8)) * 16) + (k % 8) * 2);
+}
 
 // Returns false with a message on invalid input.
 bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* hp,
@@ -68,9 +89,12 @@ struct LaunchArgs {
   const float* norms_in;
   double* sums;
   void* stream;
+  const uint8_t* qjl_img;   // device UMMA image of S (stage 2)
+  uint8_t* qjl;             // [n, d/8] sketch sign bits (stage 2)
+  float* rnorms;            // [n] residual norms (stage 2)
 };
 
-enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3 };
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4 };
 
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.

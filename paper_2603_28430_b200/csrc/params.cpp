@@ -286,4 +286,54 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
   return true;
 }
 
+// ---------------------------------------------------------------- stage 2
+// Sketch matrix of the residual correction (R20): S is
+// m x d with m = d, S[i][k] = fp16_rn(N_(i*d + k)) where N_j is the j-th
+// standard normal of the parameter generator [R12] keyed with
+// seed ^ kQjlStreamKey.  The fp16-rounded values ARE the sketch (both the
+// kernels and the oracle use them exactly).
+namespace {
+constexpr uint64_t kQjlStreamKey = 0x514A4C534B455443ull;
+
+// IEEE binary16 bits of x, rounded to nearest even directly from double.
+uint16_t half_rn(double x) {
+  uint16_t sign = std::signbit(x) ? 0x8000 : 0;
+  double a = std::fabs(x);
+  if (std::isnan(a)) return 0x7E00;
+  if (a >= 65520.0) return sign | 0x7C00;                     // rounds to infinity
+  if (a < std::ldexp(1.0, -14)) {                              // subnormal (or zero)
+    const double q = std::nearbyint(a * std::ldexp(1.0, 24));  // units of 2^-24
+    return sign | static_cast<uint16_t>(q);                    // q == 1024 -> min normal
+  }
+  int e;
+  std::frexp(a, &e);                                           // a = f * 2^e, f in [0.5, 1)
+  e -= 1;                                                      // a in [2^e, 2^(e+1))
+  double q = std::nearbyint(std::ldexp(a, 10 - e));            // [1024, 2048]
+  if (q >= 2048.0) { q = 1024.0; ++e; }
+  if (e > 15) return sign | 0x7C00;
+  return sign | static_cast<uint16_t>(((e + 15) << 10) | (static_cast<int>(q) - 1024));
+}
+}  // namespace
+
+bool qjl_supported(int d) { return d == 64 || d == 128; }
+
+bool build_qjl(HostParams* hp, std::string* err) {
+  const int d = hp->d, m = d;
+  if (d <= 0 || d % 8 != 0) { *err = "stage-2 sketch needs d % 8 == 0"; return false; }
+  const uint64_t s = hp->seed ^ kQjlStreamKey;
+  hp->qjl_half.assign(static_cast<size_t>(m) * d, 0);
+  for (int i = 0; i < m; ++i)
+    for (int k = 0; k < d; ++k)
+      hp->qjl_half[static_cast<size_t>(i) * d + k] = half_rn(normal_at(s, static_cast<uint64_t>(i) * d + k));
+  hp->qjl_img.clear();
+  if (qjl_supported(d)) {
+    hp->qjl_img.assign(static_cast<size_t>(m) * d * 2, 0);
+    for (int i = 0; i < m; ++i)
+      for (int k = 0; k < d; ++k)
+        std::memcpy(&hp->qjl_img[umma_sw128_off(i, k, m)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
+  }
+  hp->has_qjl = true;
+  return true;
+}
+
 }  // namespace iq

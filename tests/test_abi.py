@@ -127,3 +127,16 @@ def test_block_operator_is_the_sandwich_map(iq, variant):
             else:
                 col = O.forward_blocks(variant, po.qL[b:b + 1], None if po.qR is None else po.qR[b:b + 1], None, e)
             assert np.allclose(M[b][:, j], col.reshape(-1), atol=6e-8, rtol=0)
+
+
+def test_qjl_sketch_generator_matches_oracle(iq):
+    """The C++ stage-2 sketch generator (params.cpp, R20) and the oracle's
+    independent re-derivation give the same fp16 matrix."""
+    from oracle import qjl_oracle as Q
+    for d in (16, 64):
+        p = iq.iq_make_params_qjl(d, 3, iq.FULL, 20260331, device=-1)
+        assert np.array_equal(iq.iq_export_qjl_matrix(p).astype(np.float64), Q.sketch_matrix(d, 20260331))
+    assert iq.iq_qjl_bytes_per_vector(128) == 16
+    p = iq.iq_make_params(64, 3, iq.FULL, 1, device=-1)
+    with pytest.raises(iq.IQError):
+        iq.iq_export_qjl_matrix(p)
