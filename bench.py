@@ -154,7 +154,8 @@ def read_traffic(key: str):
 def bytes_per_vector(kind: str, d: int, bits: int, s: int) -> int:
     code = (d * bits + 7) // 8
     return {"roundtrip": 2 * d * s, "roundtrip_emit": 2 * d * s + code + 4,
-            "quantize": d * s + code + 4, "dequantize": code + 4 + d * s}[kind]
+            "quantize": d * s + code + 4, "dequantize": code + 4 + d * s,
+            "quantize_qjl": d * s + code + 4 + d // 8 + 4}[kind]
 
 
 def time_launches(torch, fn, reps: int, warm: int, stream) -> float:
@@ -359,6 +360,17 @@ def main():
             b = a.n * bytes_per_vector(name, a.d, a.bits, s)
             kern[name] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
                           "bytes_per_launch": b, "vectors_per_s": a.n / (t / 1e3)}
+        if a.d in (64, 128):   # stage-2 residual sketch (tcgen05), NEXT row 1
+            pq = iq.iq_make_params_qjl(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=local)
+            qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device=dev)
+            rn = torch.empty(a.n, dtype=torch.float32, device=dev)
+            t = time_launches(torch, lambda i: iq.iq_quantize_qjl(pq, xs[i & 1], codes, norms, qj, rn,
+                                                                  stream=stream), max(10, a.steps), 3, stream)
+            b = a.n * bytes_per_vector("quantize_qjl", a.d, a.bits, s)
+            kern["quantize_qjl"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                                    "bytes_per_launch": b, "vectors_per_s": a.n / (t / 1e3),
+                                    "tensor_tflops": a.n * 4 * a.d * a.d / (t / 1e3) / 1e12}
+            del qj, rn
         out["kernels"] = kern
         del codes, norms
 

@@ -26,7 +26,16 @@ namespace iq {
 template <class T, int D, int BITS, int VAR>
 struct QGeo {
   using Gm = Geo<T, D, BITS, VAR, 2>;            // stage-1 lane geometry of the code-emitting kernels
-  static constexpr int NWC = 8;                  // compute warps
+#ifdef IQ_QJL_NWC
+  static constexpr int NWC0 = IQ_QJL_NWC;
+#else
+  // measured: 16 warps (96-register cap, small spills) win at b <= 2 fp16, 8
+  // warps (no spills) elsewhere
+  static constexpr int NWC0 = (sizeof(T) == 2 && BITS <= 2) ? 16 : 8;
+#endif
+  // compute warps: a multiple of 4 (TMEM lane quadrants), each with at least
+  // one row pair per lane group of the 128-row tile
+  static constexpr int NWC = NWC0 < 128 / (2 * Gm::VPW) ? NWC0 : 128 / (2 * Gm::VPW);
   static constexpr int CTA_THREADS = 32 * (NWC + 2);   // + TMA producer + MMA warp
   static constexpr int TILE = 128;               // rows per tile = UMMA M
   static constexpr int M = D;                    // sketch rows (m = d, R20)
@@ -38,11 +47,14 @@ struct QGeo {
   static constexpr int A_OFF = NST * STAGE;      // 1024-aligned (STAGE is)
   static constexpr int S_OFF = A_OFF + 2 * A_BYTES;
   static constexpr int BAR_OFF = S_OFF + S_BYTES;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;   // + slack to align the base to 1024
+  static constexpr int OPS_OFF = BAR_OFF + 256;   // stage-1 operators (when Gm::OPS_SMEM)
+  static constexpr int SMEM = OPS_OFF + Gm::OPS_BYTES + 1024;   // + slack to align the base to 1024
+  static constexpr int CW = M / (NWC / 4);        // sketch columns per epilogue warp
   static constexpr int TMEM_COLS = (2 * M) <= 32 ? 32 : (2 * M) <= 64 ? 64 : (2 * M) <= 128 ? 128 : 256;
   static constexpr int U = TILE / (NWC * Gm::VPW);   // rows per lane group per tile
   static_assert(U % 2 == 0, "row pairs");
   static_assert(D == 64 || D == 128, "sketch kernel: d in {64, 128}");
+  static_assert(NWC % 4 == 0 && (CW == 16 || CW % 32 == 0), "epilogue split");
 };
 
 // ------------------------------------------------------------ tcgen05 helpers
@@ -72,9 +84,10 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// 32 consecutive fp32 columns of this thread's TMEM lane -> sign word:
-// bit j = [z_j >= 0] (the float sign bit, so -0 counts as negative; R22).
-__device__ __forceinline__ uint32_t tmem_sign_word(uint32_t taddr) {
+// 32 (or 16) consecutive fp32 columns of this thread's TMEM lane -> sign
+// word: bit j = [z_j >= 0], taken from the float sign bit (R22; a -0 result
+// needs every product to be -0, which the zero row does not produce).
+__device__ __forceinline__ uint32_t tmem_sign_word32(uint32_t taddr) {
   uint32_t v[32];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -90,6 +103,20 @@ __device__ __forceinline__ uint32_t tmem_sign_word(uint32_t taddr) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) neg |= (v[j] >> 31) << j;
   return ~neg;
+}
+__device__ __forceinline__ uint32_t tmem_sign_word16(uint32_t taddr) {
+  uint32_t v[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  uint32_t neg = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) neg |= (v[j] >> 31) << j;
+  return ~neg & 0xFFFFu;
 }
 
 // store fp16 hi / lo of a lane's EPC consecutive coordinates of tile row r
@@ -207,13 +234,23 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
     const int sub = lane & (G - 1);
     const int vbase = lane & ~(G - 1);
     const int vslot = lane / G;
-    float P[NBL][PW * PW];
-    load_ops<Gm>(mat, sub, P);
+    float P[Gm::OPS_SMEM ? 1 : NBL][PW * PW];
+    uint8_t* const ops = smem + Q::OPS_OFF;
+    if constexpr (Gm::OPS_SMEM) {
+      if (warp == 0 && lane < G) {
+        float Pl[NBL][PW * PW];
+        load_ops<Gm>(mat, sub, Pl);
+        store_ops_smem<Gm>(ops, sub, Pl);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // compute warps only
+    } else {
+      load_ops<Gm>(mat, sub, P);
+    }
     const float ctab = cb.cent[lane & ((1 << BITS) - 1)];
     const float gtab = cb.gtab[lane];
     const uint32_t gcode = cb.gcode[lane];
-    const int quad = warp & 3, half = warp >> 2;      // TMEM lane quadrant, column half
-    constexpr int HC = M / 2;                         // columns per epilogue warp
+    const int quad = warp & 3, part = warp >> 2;      // TMEM lane quadrant, column slice
+    constexpr int CW = Q::CW;                         // columns per epilogue warp
 
     auto epilogue = [&](uint32_t jj, int64_t tt) {
       const uint32_t b = jj & 1;
@@ -221,17 +258,22 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
       tc_fence_after();
       const int row = 32 * quad + lane;
       const int64_t v = tt * TILE + row;
-      uint32_t w[HC / 32];
+      const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16) + b * M + part * CW;
+      uint32_t w[CW >= 32 ? CW / 32 : 1];
+      if constexpr (CW == 16) {
+        w[0] = tmem_sign_word16(ta);
+      } else {
 #pragma unroll
-      for (int c = 0; c < HC / 32; ++c)
-        w[c] = tmem_sign_word(tmem + ((uint32_t)(32 * quad) << 16) + b * M + half * HC + 32 * c);
+        for (int c = 0; c < CW / 32; ++c) w[c] = tmem_sign_word32(ta + 32 * c);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
       if (v < n) {
-        uint8_t* dst = qjl + v * (M / 8) + half * (HC / 8);
-        if constexpr (HC / 32 == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-        else *reinterpret_cast<uint32_t*>(dst) = w[0];
+        uint8_t* dst = qjl + v * (M / 8) + part * (CW / 8);
+        if constexpr (CW == 16) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)w[0];
+        else if constexpr (CW == 32) *reinterpret_cast<uint32_t*>(dst) = w[0];
+        else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
       }
     };
 
@@ -248,8 +290,6 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
       uint8_t* const ct = codes + v0 * RB;
       float* const nt = norms + v0;
       float* const gt = rnorms + v0;
-      // the A tiles of the previous tile must have been consumed by its MMAs
-      mbar_wait(a_free, (j & 1) ^ 1);
 #pragma unroll 1
       for (int u = 0; u < U; u += 2) {
         uint4 ra[CPL], rb[CPL];
@@ -286,9 +326,11 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
 #pragma unroll
           for (int b = 0; b < NBL; ++b) {
             float2 xs[PW], yb[PW], cq[PW];
+            float Mb[PW * PW];
+            fetch_op<Gm>(P, ops, sub, b, Mb);
 #pragma unroll
             for (int jv = 0; jv < PW; ++jv) xs[jv] = mul2(v[b * PW + jv], sc);
-            rot_fwd<PW>(P[b], xs, yb);
+            rot_fwd<PW>(Mb, xs, yb);
 #pragma unroll
             for (int jv = 0; jv < PW; ++jv) {
               const uint32_t ia = grid_index(yb[jv].x, gtab, cb.gclamp);
@@ -299,9 +341,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
               cq[jv] = f2(sign_xor(__shfl_sync(kFull, gtab, (int)ia), yb[jv].x),
                           sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[jv].y));
             }
-            rot_inv<PW>(P[b], cq, out + b * PW);
-#pragma unroll
-            for (int jv = 0; jv < PW; ++jv) out[b * PW + jv] = mul2(out[b * PW + jv], rho);
+            rot_inv<PW>(Mb, cq, out + b * PW);          // T^-1(C[code]); rho applied with r below
           }
         } else {
           RowQ<BITS> q;
@@ -310,20 +350,19 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
 #pragma unroll
           for (int i = 0; i < CPL; ++i) {
             float2 yb[EPC], cq[EPC];
+            float Mc[BPCH][PW * PW];
 #pragma unroll
-            for (int bb = 0; bb < BPCH; ++bb) rot_fwd<PW>(P[i * BPCH + bb], v + i * EPC + bb * PW, yb + bb * PW);
+            for (int bb = 0; bb < BPCH; ++bb) {
+              fetch_op<Gm>(P, ops, sub, i * BPCH + bb, Mc[bb]);
+              rot_fwd<PW>(Mc[bb], v + i * EPC + bb * PW, yb + bb * PW);
+            }
             encode_chunk<BITS, EPC>(yb, q, cwa[i], cwb[i]);
 #pragma unroll
             for (int e = 0; e < EPC; ++e)
               cq[e] = f2(__shfl_sync(kFull, ctab, (int)(cwa[i] >> (e * BITS)), 1 << BITS),
                          __shfl_sync(kFull, ctab, (int)(cwb[i] >> (e * BITS)), 1 << BITS));
 #pragma unroll
-            for (int bb = 0; bb < BPCH; ++bb) {
-              float2* o = out + i * EPC + bb * PW;
-              rot_inv<PW>(P[i * BPCH + bb], cq + bb * PW, o);
-#pragma unroll
-              for (int jv = 0; jv < PW; ++jv) o[jv] = mul2(o[jv], rho);
-            }
+            for (int bb = 0; bb < BPCH; ++bb) rot_inv<PW>(Mc[bb], cq + bb * PW, out + i * EPC + bb * PW);
           }
         }
         // codes + norms (bit-identical to iq_quantize)
@@ -337,11 +376,12 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
             if (okb) *reinterpret_cast<uint32_t*>(ct + off + VPW * RB) = wb;
           }
         }
-        // ---- residual r = x - x^ (R21), gamma = ||r|| (R23)
+        // ---- residual r = x - rho T^-1(C[code]) (R21), gamma = ||r|| (R23)
+        const float2 nrho = f2(-rho.x, -rho.y);
         float2 g2 = bc(0.0f);
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
-          out[e] = add2(v[e], f2(-out[e].x, -out[e].y));
+          out[e] = fma2(out[e], nrho, v[e]);
           g2 = fma2(out[e], out[e], g2);
         }
 #pragma unroll
@@ -353,6 +393,9 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         }
         // ---- UMMA A operand: r * 256 / max(rho, eps) as fp16 hi + lo (sign(S r) is scale-free)
         const float2 sr = mul2(rinv, bc(256.0f));
+        // the previous tile's MMAs must have consumed the A tiles (the
+        // stage-1 work above overlaps them)
+        if (u == 0) mbar_wait(a_free, (j & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           float ta[EPC], tb[EPC];

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kernel", default="roundtrip",
-                    choices=["roundtrip", "roundtrip_emit", "quantize", "dequantize", "all"])
+                    choices=["roundtrip", "roundtrip_emit", "quantize", "dequantize", "quantize_qjl", "all"])
     ap.add_argument("--variant", default="full")
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--bits", type=int, default=3)
@@ -31,6 +31,10 @@ def main():
     codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
     norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
     iq.iq_quantize(p, x, codes, norms)
+    if a.kernel == "quantize_qjl":
+        pq = iq.iq_make_params_qjl(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
+        qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device="cuda")
+        rn = torch.empty(a.n, dtype=torch.float32, device="cuda")
     kinds = ["quantize", "dequantize", "roundtrip", "roundtrip_emit"] if a.kernel == "all" else [a.kernel]
     for k in kinds:
         for _ in range(a.reps):
@@ -40,6 +44,8 @@ def main():
                 iq.iq_roundtrip(p, x, y=y, codes=codes, norms=norms)
             elif k == "quantize":
                 iq.iq_quantize(p, x, codes, norms)
+            elif k == "quantize_qjl":
+                iq.iq_quantize_qjl(pq, x, codes, norms, qj, rn)
             else:
                 iq.iq_dequantize(p, codes, norms, y=y)
     torch.cuda.synchronize()

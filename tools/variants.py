@@ -17,10 +17,7 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "opsreg": ["-DIQ_OPS_SMEM=0"],          # operators always in registers (8-warp CTAs)
-    "nwc12": ["-DIQ_NWC_WIDE=12"],          # 12 compute warps in the wide encoder CTAs
-    "b3fma": ["-DIQ_B3_ALU=0"],             # b = 3 chain as FSET + FFMA2
-    "stage64": ["-DIQ_STAGE_KB=64"],        # 64 KB ring stages
+    "qjl8": ["-DIQ_QJL_NWC=8"],
 }
 
 
@@ -50,6 +47,10 @@ def time_one(a):
     norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
     iq.iq_quantize(p, xs[0], codes, norms)
     cb = p.code_bytes
+    if a.d in (64, 128):
+        pq = iq.iq_make_params_qjl(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
+        qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device="cuda")
+        rn = torch.empty(a.n, dtype=torch.float32, device="cuda")
     out = {}
     for name, fn, bpv in [
         ("rt", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1]), 2 * a.d * s),
@@ -57,7 +58,8 @@ def time_one(a):
         ("dq", lambda i: iq.iq_dequantize(p, codes, norms, y=ys[i & 1]), a.d * s + cb + 4),
         ("rte", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], codes=codes, norms=norms),
          2 * a.d * s + cb + 4),
-    ]:
+    ] + ([("qjl", lambda i: iq.iq_quantize_qjl(pq, xs[i & 1], codes, norms, qj, rn), a.d * s + cb + 8 + a.d // 8)]
+         if a.d in (64, 128) else []):
         for i in range(5):
             fn(i)
         torch.cuda.synchronize()
