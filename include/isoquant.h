@@ -221,6 +221,29 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
                           void* cuda_stream);
 
 /*
+ * iq_attention_scores — fused KV-cache decode consumer (
+ * DESIGN.md R25-R27): attention logits straight from the packed cache,
+ *   scores[h][j][k] = <q_hj, x^_hk> = rho_hk <T q_hj, C[code_hk]>
+ *                   (+ sqrt(pi/2)/m * gamma_hk * <S q_hj, sign_hk> if qjl != NULL)
+ * for `heads` independent heads sharing the handle, n_keys keys and n_q
+ * queries (1..16) per head.  No key is inverse-rotated: queries are rotated
+ * once per head, keys are only decoded; the dot products run on the tensor
+ * cores (tcgen05, fp16 operands, fp32 accumulation).
+ *  codes  : [heads, n_keys, code bytes]   norms  : [heads, n_keys] float
+ *  qjl    : [heads, n_keys, d/8] or NULL  rnorms : [heads, n_keys] or NULL
+ *           (both set: the stage-2 estimate; needs iq_make_params_qjl)
+ *  q      : [heads, n_q, d] of q_dtype      scores : [heads, n_q, n_keys] float
+ * Precision: fp16 centroids and queries (per-query power-of-two scaling):
+ * |error| <= ~1e-3 * rho_hk * ||q_hj|| (stage 1), see DESIGN.md.  d in
+ * {64, 128}.  codes, norms, qjl, rnorms 16-byte aligned; with heads > 1,
+ * n_keys % 4 == 0 (else MISALIGNED).
+ */
+iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_t n_keys,
+                              const uint8_t* codes, const float* norms, const uint8_t* qjl,
+                              const float* rnorms, int n_q, const void* q, float* scores,
+                              void* cuda_stream);
+
+/*
  * iq_error_sums — reconstruction statistics on the device (not part of the
  * timed path): sums[0] += sum_{i,j} (x_ij - y_ij)^2, sums[1] += sum x_ij^2,
  * accumulated in fp64 with atomics into the DEVICE buffer sums[2] (caller

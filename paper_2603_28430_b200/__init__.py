@@ -23,6 +23,7 @@ __all__ = [
     "iq_export_params", "iq_export_block_matrices", "iq_code_bytes_per_vector",
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
     "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
+    "iq_attention_scores",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -61,6 +62,8 @@ _sig = {
     "iq_qjl_bytes_per_vector": (_c_sz, [_c_int]),
     "iq_export_qjl_matrix": (_c_int, [_c_vp, _c_vp, _c_sz]),
     "iq_quantize_qjl": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_attention_scores": (_c_int, [_c_vp, _c_int, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_vp,
+                                     _c_vp, _c_vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -257,6 +260,33 @@ def iq_quantize_qjl(p: Params, x, codes=None, norms=None, qjl=None, rnorms=None,
     _check(lib.iq_quantize_qjl(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms), _ptr(qjl),
                                _ptr(rnorms), _stream_ptr(stream)), "iq_quantize_qjl")
     return codes, norms, qjl, rnorms
+
+
+def iq_attention_scores(p: Params, codes, norms, q, qjl=None, rnorms=None, scores=None, stream=None):
+    """Attention logits from the packed cache.  codes [H, N, code bytes] (or
+    [N, bytes] for H = 1), norms [H, N]; q [H, n_q, d] (f32/f16, the handle's
+    I/O dtype of the call); optional stage-2 qjl [H, N, d/8] + rnorms [H, N].
+    Returns scores [H, n_q, N] float32."""
+    torch = _torch()
+    if codes.dim() == 2:
+        codes, norms = codes.unsqueeze(0), norms.unsqueeze(0)
+        if qjl is not None:
+            qjl, rnorms = qjl.unsqueeze(0), rnorms.unsqueeze(0)
+    if q.dim() == 2:
+        q = q.unsqueeze(0)
+    H, N = codes.shape[0], codes.shape[1]
+    n_q = q.shape[1]
+    for t in (codes, norms, q) + ((qjl, rnorms) if qjl is not None else ()):
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+    if q.shape[0] != H or q.shape[2] != p.d:
+        raise ValueError(f"q must be [{H}, n_q, {p.d}]")
+    if scores is None:
+        scores = torch.empty((H, n_q, N), dtype=torch.float32, device=codes.device)
+    _check(lib.iq_attention_scores(p.handle, _dtype_code(q), H, N, _ptr(codes), _ptr(norms), _ptr(qjl),
+                                   _ptr(rnorms), n_q, _ptr(q), _ptr(scores), _stream_ptr(stream)),
+           "iq_attention_scores")
+    return scores
 
 
 def iq_error_sums(p: Params, x, y, sums=None, stream=None):

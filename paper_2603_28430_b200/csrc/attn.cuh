@@ -1,0 +1,376 @@
+// Fused KV-cache decode consumer (NEXT row 2 of SURVEY section 8(f);
+// PAPER.md:460 "attention-logit preservation and inner-product error under
+// the complete two-stage pipeline", "specialized kernels for fused
+// KV-cache compression during autoregressive decoding").  DESIGN.md R25-R27.
+//
+// Attention logits straight from the packed cache, for H independent heads
+// (one parameter handle, R13) of n_keys keys each and up to 16 queries per
+// head (a GQA group or a batch of decode steps):
+//   s[h][j][k] = <q_hj, x^_hk> = rho_hk <T q_hj, C[code_hk]>        (T orthogonal)
+//              + sqrt(pi/2)/m gamma_hk <S q_hj, sign_hk>            (stage 2, optional)
+// so no key is ever inverse-rotated: the queries are rotated once per head
+// and the keys only decoded.  Per 128-key tile:
+//   decoder warps (4, thread = key row) : TMA-staged codes (+ sketch bits)
+//       -> C[code] as fp16 (width-L shuffle table) and +-1 fp16 from the
+//       sketch bits (width-4 shuffle table of half2 pairs), written to
+//       K-major 128B-swizzled UMMA A tiles;
+//   MMA warp (one elected thread)       : tcgen05.mma kind::f16, M = 128 keys,
+//       N = 16 query slots, K = d, into TMEM (stage-1 and stage-2 accumulators);
+//   decoder warps, one tile later       : tcgen05.ld, scale by rho_k / sigma_j
+//       (+ gamma_k sqrt(pi/2)/m / tau_j), store s[h][j][k] (coalesced in k).
+#pragma once
+#include "qjl.cuh"
+
+namespace iq {
+
+template <int D, int BITS>
+struct AGeo {
+  static constexpr int NQ = 16;                  // query slots (UMMA N)
+  static constexpr int TILE = 128;               // keys per tile (UMMA M)
+  static constexpr int RB = D * BITS / 8;        // code bytes per key
+  static constexpr int QB = D / 8;               // sketch bytes per key
+  // ring stage: codes [TILE][RB] | norms [TILE] | sketch [TILE][QB] | gammas [TILE]
+  static constexpr int C_OFF = 0;
+  static constexpr int N_OFF = (TILE * RB + 15) / 16 * 16;
+  static constexpr int Q_OFF = N_OFF + TILE * 4;
+  static constexpr int G_OFF = Q_OFF + TILE * QB;
+  static constexpr int STAGE = (G_OFF + TILE * 4 + 1023) / 1024 * 1024;
+  static constexpr int NST = 3;
+  static constexpr int A_BYTES = TILE * D * 2;   // one fp16 A tile
+  static constexpr int B_BYTES = NQ * D * 2;     // one fp16 B tile (queries)
+  static constexpr int A_OFF = NST * STAGE;      // [2 buffers][stage 1, stage 2]
+  static constexpr int B_OFF = A_OFF + 4 * A_BYTES;
+  static constexpr int QT_OFF = B_OFF + 2 * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
+  static constexpr int S_OFF = QT_OFF + B_BYTES;        // S image, 128 rows (A of the S q MMA)
+  static constexpr int S_BYTES = 128 * D * 2;
+  static constexpr int BAR_OFF = S_OFF + S_BYTES;
+  static constexpr int SC_OFF = BAR_OFF + 256;   // per-query scales [2][NQ] floats
+  static constexpr int SMEM = SC_OFF + 2 * NQ * 4 + 1024;
+  static constexpr int NWD = 4;                  // decoder / epilogue warps (TMEM lane quadrants)
+  static constexpr int CTA_THREADS = 32 * (NWD + 2);
+  static constexpr int TMEM_COLS = 128;          // [2 buffers][stage 1, stage 2] x NQ, + NQ for S q
+  static constexpr int SQ_COL = 4 * NQ;
+  static_assert(D == 64 || D == 128, "attention consumer: d in {64, 128}");
+};
+
+__device__ __forceinline__ uint32_t tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr));
+  return 0;
+}
+
+template <class TQ, int D, int BITS, int VAR>
+__global__ void __launch_bounds__(AGeo<D, BITS>::CTA_THREADS, 1)
+k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int64_t n_keys,
+              const uint8_t* __restrict__ codes, const float* __restrict__ norms,
+              const uint8_t* __restrict__ sketch, const float* __restrict__ gammas,
+              const uint8_t* __restrict__ s_img, int n_q, const TQ* __restrict__ q, float* __restrict__ scores) {
+  using A = AGeo<D, BITS>;
+  constexpr int TILE = A::TILE, NQ = A::NQ, NWD = A::NWD, NST = A::NST, RB = A::RB, QB = A::QB;
+  constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;
+  constexpr int L = 1 << BITS;
+  const bool st2 = sketch != nullptr;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* a_base = smem + A::A_OFF;            // A[buf][part] at a_base + (2 buf + part) A_BYTES
+  uint8_t* b_base = smem + A::B_OFF;            // B[part]
+  float* qscale = reinterpret_cast<float*>(smem + A::SC_OFF);   // [2][NQ]: 1/sigma_j, 1/tau_j
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
+  uint64_t* empty = full + NST;
+  uint64_t* a_full = empty + NST;    // [2]
+  uint64_t* a_free = a_full + 2;     // [2]
+  uint64_t* acc_full = a_free + 2;   // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint64_t* s_bar = acc_empty + 2;     // S image loaded
+  uint64_t* sq_bar = s_bar + 1;        // S q MMA done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_bar + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWD); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1);
+      mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], NWD);
+    }
+    mbar_init(s_bar, 1);
+    mbar_init(sq_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == NWD + 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(A::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t tph = (n_keys + TILE - 1) / TILE;   // tiles per head
+  const int64_t ntiles = tph * heads;
+
+  if (warp == NWD) {  // ---------------------------------------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      if (st2) {
+        mbar_arrive_expect_tx(s_bar, A::S_BYTES);
+        bulk_g2s(smem + A::S_OFF, s_img, A::S_BYTES, s_bar, policy_evict_last());
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
+        const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
+        const int64_t row0 = h * n_keys + k0;
+        // whole 16-byte units; a ragged remainder is read from global memory
+        const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
+        const uint32_t qb16 = st2 ? ((uint32_t)(nk * QB) & ~15u) : 0u, gb16 = st2 ? nb16 : 0u;
+        const uint32_t tot = cb16 + nb16 + qb16 + gb16;
+        uint8_t* stg = smem + s * A::STAGE;
+        if (tot == 0) {
+          mbar_arrive(&full[s]);
+        } else {
+          mbar_arrive_expect_tx(&full[s], tot);
+          if (cb16) bulk_g2s(stg + A::C_OFF, codes + row0 * RB, cb16, &full[s], pol);
+          if (nb16) bulk_g2s(stg + A::N_OFF, norms + row0, nb16, &full[s], pol);
+          if (qb16) bulk_g2s(stg + A::Q_OFF, sketch + row0 * QB, qb16, &full[s], pol);
+          if (gb16) bulk_g2s(stg + A::G_OFF, gammas + row0, gb16, &full[s], pol);
+        }
+        if (++s == NST) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == NWD + 1) {  // ------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
+      const uint32_t ab = smem_u32(a_base), bb = smem_u32(b_base);
+      uint32_t j = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        const uint32_t b = j & 1;
+        mbar_wait(&a_full[b], (j >> 1) & 1);
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int part = 0; part < (st2 ? 2 : 1); ++part) {
+          const uint32_t ta = ab + (2 * b + part) * A::A_BYTES, tb = bb + part * A::B_BYTES;
+          const uint32_t td = tmem + (2 * b + part) * NQ;
+#pragma unroll
+          for (int s = 0; s < D / 16; ++s)
+            umma_f16(td, umma_desc_sw128(ta + umma_kstep_off(s, TILE)), umma_desc_sw128(tb + umma_kstep_off(s, NQ)),
+                     idesc, s != 0);
+        }
+        umma_commit(&a_free[b]);
+        umma_commit(&acc_full[b]);
+      }
+    }
+  } else {  // ------------------------------------------- decoder / epilogue warps
+    const int row = 32 * warp + lane;            // key row of the tile = TMEM lane
+    const float ctab = cb.cent[lane & (L - 1)];  // C[l] in lane l of each group of L
+    // +-1 fp16 pairs for 2 sketch bits (bit set = +1, R22): lane l holds the
+    // half2 for bits (l & 3)
+    const uint32_t ptab = ((lane & 1) ? 0x3C00u : 0xBC00u) | ((lane & 2) ? 0x3C000000u : 0xBC000000u);
+    const float cpi = 1.2533141373155003f / (float)D;   // sqrt(pi/2) / m, m = d (R20)
+
+    // rotate the head's queries into the B tiles: q' = T q (stage 1) and
+    // S q (stage 2), fp16 with per-query power-of-two scales
+    uint32_t nprep = 0;                          // query preparations so far (sq_bar parity)
+    auto load_queries = [&](int64_t h) {
+      const TQ* qh = q + h * (int64_t)n_q * D;
+      if (threadIdx.x < NQ) {
+        const int jq = threadIdx.x;
+        float ss = 0.0f;
+        if (jq < n_q)
+          for (int i = 0; i < D; ++i) { const float v = (float)qh[jq * D + i]; ss = fmaf(v, v, ss); }
+        // sigma = 2^(8 - ceil(log2 ||q||)): |T q| <= ||q|| -> |sigma T q| <= 256;
+        // the stage-2 tile holds S sigma q / 8 (|.| <~ 4 sqrt(d) 256 / 8)
+        int e = 0;
+        frexpf(sqrtf(ss), &e);
+        qscale[jq] = ldexpf(1.0f, e - 8);                 // 1 / sigma
+        qscale[NQ + jq] = ldexpf(1.0f, e - 5);            // 8 / sigma
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
+      // stage 1: thread handles (query jq, block b)
+      for (int w = threadIdx.x; w < NQ * (D / PW); w += NWD * 32) {
+        const int jq = w / (D / PW), b = w % (D / PW);
+        float xv[PW], yv[PW];
+        const float sg = 1.0f / qscale[jq];
+#pragma unroll
+        for (int c = 0; c < PW; ++c) xv[c] = jq < n_q ? (float)qh[jq * D + b * PW + c] * sg : 0.0f;
+#pragma unroll
+        for (int r = 0; r < PW; ++r) {
+          float a = 0.0f;
+#pragma unroll
+          for (int c = 0; c < PW; ++c) a = fmaf(__ldg(mat + (size_t)b * PW * PW + r * PW + c), xv[c], a);
+          yv[r] = a;
+        }
+#pragma unroll
+        for (int r = 0; r < PW; ++r)
+          *reinterpret_cast<__half*>(b_base + umma_sw128_off(jq, b * PW + r, NQ)) = __float2half_rn(yv[r]);
+      }
+      if (st2) {
+        // stage 2: S q on the tensor cores.  B = sigma q as fp16 (queries x d),
+        // A = S (128 x d, rows >= m zero), D = S (sigma q)^T in TMEM; thread i
+        // then holds (S sigma q_j)_i for the 16 query slots and writes
+        // (S sigma q_j)_i / 8 into the stage-2 B tile (row j, column i)
+        for (int w = threadIdx.x; w < NQ * D; w += NWD * 32) {
+          const int jq = w / D, k = w % D;
+          const float v = jq < n_q ? (float)qh[jq * D + k] / qscale[jq] : 0.0f;
+          *reinterpret_cast<__half*>(smem + A::QT_OFF + umma_sw128_off(jq, k, NQ)) = __float2half_rn(v);
+        }
+        fence_async_smem();
+        asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
+        if (threadIdx.x == 0) {
+          mbar_wait(s_bar, 0);
+          tc_fence_after();
+          const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+          const uint32_t sa = smem_u32(smem + A::S_OFF), qb = smem_u32(smem + A::QT_OFF);
+#pragma unroll
+          for (int s = 0; s < D / 16; ++s)
+            umma_f16(tmem + A::SQ_COL, umma_desc_sw128(sa + umma_kstep_off(s, 128)),
+                     umma_desc_sw128(qb + umma_kstep_off(s, NQ)), idesc, s != 0);
+          umma_commit(sq_bar);
+        }
+        mbar_wait(sq_bar, nprep & 1);
+        tc_fence_after();
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + A::SQ_COL, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        const int i = 32 * warp + lane;
+        if (i < D) {
+#pragma unroll
+          for (int jq = 0; jq < NQ; ++jq)
+            *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
+                __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
+        }
+      }
+      ++nprep;
+      fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
+    };
+
+    auto epilogue = [&](uint32_t jj, int64_t tt, float rho, float gam) {
+      const uint32_t b = jj & 1;
+      mbar_wait(&acc_full[b], (jj >> 1) & 1);
+      tc_fence_after();
+      uint32_t v1[16], v2[16];
+      const uint32_t lanes = (uint32_t)(32 * warp) << 16;
+      tmem_ld16(tmem + lanes + (2 * b) * NQ, v1);
+      if (st2) tmem_ld16(tmem + lanes + (2 * b + 1) * NQ, v2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      const int64_t h = tt / tph, k = (tt - h * tph) * TILE + row;
+      if (k < n_keys) {
+        float* out = scores + h * (int64_t)n_q * n_keys + k;
+#pragma unroll
+        for (int jq = 0; jq < NQ; ++jq) {
+          if (jq < n_q) {
+            float sv = __uint_as_float(v1[jq]) * qscale[jq] * rho;
+            if (st2) sv = fmaf(__uint_as_float(v2[jq]) * qscale[NQ + jq], cpi * gam, sv);
+            out[(int64_t)jq * n_keys] = sv;
+          }
+        }
+      }
+    };
+
+    int s = 0;
+    uint32_t ph = 0, j = 0;
+    int64_t tprev = -1, hcur = -1;
+    float rho_prev = 0.0f, gam_prev = 0.0f;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
+      if (h != hcur) {               // drain the MMAs that read the previous head's queries
+        if (tprev >= 0) { epilogue(j - 1, tprev, rho_prev, gam_prev); tprev = -1; }
+        load_queries(h);
+        hcur = h;
+      }
+      mbar_wait(&full[s], ph);
+      const uint8_t* stg = smem + s * A::STAGE;
+      const int ss_ = s;
+      if (++s == NST) { s = 0; ph ^= 1; }
+      const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
+      const bool valid = row < nk;
+      const int64_t grow = h * n_keys + k0 + row;
+      const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
+      const uint32_t qb16 = (uint32_t)(nk * QB) & ~15u;
+      // this key's code words, norm, sketch words and gamma (smem, or global for a ragged tail)
+      uint32_t cw[RB / 4];
+#pragma unroll
+      for (int i = 0; i < RB / 4; ++i)
+        cw[i] = !valid ? 0u
+                : ((uint32_t)(row * RB + 4 * i + 4) <= cb16) ? lds32(stg + A::C_OFF + row * RB + 4 * i)
+                                                             : __ldg(reinterpret_cast<const uint32_t*>(codes + grow * RB) + i);
+      float rho = !valid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::N_OFF + row * 4) : __ldg(norms + grow);
+      uint32_t qw[QB / 4];
+      float gam = 0.0f;
+      if (st2) {
+#pragma unroll
+        for (int i = 0; i < QB / 4; ++i)
+          qw[i] = !valid ? 0u
+                  : ((uint32_t)(row * QB + 4 * i + 4) <= qb16) ? lds32(stg + A::Q_OFF + row * QB + 4 * i)
+                                                               : __ldg(reinterpret_cast<const uint32_t*>(sketch + grow * QB) + i);
+        gam = !valid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::G_OFF + row * 4) : __ldg(gammas + grow);
+      }
+      {
+        float dep = rho + gam;
+#pragma unroll
+        for (int i = 0; i < RB / 4; ++i) dep += __uint_as_float(cw[i] & 0x007FFFFFu);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
+      }
+      const uint32_t b = j & 1;
+      mbar_wait(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
+      uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
+      uint8_t* a2 = a1 + A::A_BYTES;
+      // stage 1: C[code] as fp16, 8 coordinates (16 bytes) at a time
+#pragma unroll
+      for (int c8 = 0; c8 < D / 8; ++c8) {
+        uint32_t hw[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int b0 = (c8 * 8 + e) * BITS, b1 = b0 + BITS;
+          const uint32_t s0 = (b0 % 32 + BITS <= 32) ? (cw[b0 / 32] >> (b0 % 32))
+                                                     : __funnelshift_r(cw[b0 / 32], cw[b0 / 32 + 1], b0 % 32);
+          const uint32_t s1 = (b1 % 32 + BITS <= 32) ? (cw[b1 / 32] >> (b1 % 32))
+                                                     : __funnelshift_r(cw[b1 / 32], cw[b1 / 32 + 1], b1 % 32);
+          const float v0 = __shfl_sync(kFull, ctab, (int)s0, L), v1 = __shfl_sync(kFull, ctab, (int)s1, L);
+          const __half2 hh = __floats2half2_rn(v0, v1);
+          hw[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+        }
+        *reinterpret_cast<uint4*>(a1 + umma_sw128_off(row, c8 * 8, TILE)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      }
+      if (st2) {  // stage 2: +-1 from the sketch bits, 8 at a time
+#pragma unroll
+        for (int c8 = 0; c8 < D / 8; ++c8) {
+          const uint32_t byte = qw[c8 / 4] >> ((c8 % 4) * 8);
+          uint32_t hw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__shfl_sync(kFull, (int)ptab, (int)(byte >> (2 * e)), 4);
+          *reinterpret_cast<uint4*>(a2 + umma_sw128_off(row, c8 * 8, TILE)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[b]);
+      if (tprev >= 0) epilogue(j - 1, tprev, rho_prev, gam_prev);
+      tprev = t;
+      rho_prev = rho;
+      gam_prev = gam;
+    }
+    if (tprev >= 0) epilogue(j - 1, tprev, rho_prev, gam_prev);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NWD + 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(A::TMEM_COLS));
+  }
+}
+
+}  // namespace iq

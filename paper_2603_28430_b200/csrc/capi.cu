@@ -20,6 +20,8 @@ int launch_fast_f16(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_f32(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_f16(Kernel, int, int, const LaunchArgs&);
 
+bool attn_supported(int d) { return d == 64 || d == 128; }
+
 bool gpu_supported(int d, int bits, int variant) {
   const bool dok = d == 64 || d == 128 || d == 256 || d == 512;
   return dok && bits >= 1 && bits <= kMaxBits && variant >= 0 && variant <= 2;
@@ -40,6 +42,7 @@ struct iq_params {
   int device = -1;
   float* d_mat = nullptr;
   uint8_t* d_qjl = nullptr;   // UMMA image of the stage-2 sketch S (iq_make_params_qjl)
+  uint8_t* d_qjl_a = nullptr; // the same S as a 128-row A operand (attention consumer)
 };
 
 namespace {
@@ -151,10 +154,14 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
     if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl, p->hp.qjl_img.size());
     if (e == cudaSuccess && qjl)
       e = cudaMemcpy(p->d_qjl, p->hp.qjl_img.data(), p->hp.qjl_img.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl_a, p->hp.qjl_img_a.size());
+    if (e == cudaSuccess && qjl)
+      e = cudaMemcpy(p->d_qjl_a, p->hp.qjl_img_a.data(), p->hp.qjl_img_a.size(), cudaMemcpyHostToDevice);
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
     if (e != cudaSuccess) {
       if (p->d_mat) cudaFree(p->d_mat);
       if (p->d_qjl) cudaFree(p->d_qjl);
+      if (p->d_qjl_a) cudaFree(p->d_qjl_a);
       delete p;
       return cuda_fail(e, "iq_make_params device upload");
     }
@@ -179,6 +186,7 @@ iq_status iq_free_params(iq_params* p) {
     if (prev != p->device) cudaSetDevice(p->device);
     cudaFree(p->d_mat);
     if (p->d_qjl) cudaFree(p->d_qjl);
+    if (p->d_qjl_a) cudaFree(p->d_qjl_a);
     if (prev >= 0 && prev != p->device) cudaSetDevice(prev);
   }
   delete p;
@@ -270,6 +278,40 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
   a.qjl = qjl;
   a.rnorms = rnorms;
   return run(iq::Kernel::kQuantizeQjl, p, dtype, a);
+}
+
+iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_t n_keys,
+                              const uint8_t* codes, const float* norms, const uint8_t* qjl,
+                              const float* rnorms, int n_q, const void* q, float* scores, void* stream) {
+  iq_status s = check_call(p, q_dtype, n_keys);
+  if (s != IQ_OK) return s;
+  if (!iq::attn_supported(p->hp.d))
+    return fail(IQ_ERR_UNSUPPORTED, "the attention consumer supports d in {64, 128}");
+  if (heads < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "heads must be >= 1");
+  if (n_q < 1 || n_q > 16) return fail(IQ_ERR_INVALID_ARGUMENT, "n_q must be in [1, 16]");
+  if ((qjl == nullptr) != (rnorms == nullptr))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "qjl and rnorms must be both NULL or both set");
+  if (qjl && (!p->hp.has_qjl || !p->d_qjl_a))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "stage-2 scores need a handle with the sketch (iq_make_params_qjl)");
+  if (n_keys == 0) return IQ_OK;
+  if (!codes || !norms || !q || !scores)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms, q and scores are required");
+  if (!aligned(codes, 16) || !aligned(norms, 16) || (qjl && (!aligned(qjl, 16) || !aligned(rnorms, 16))) ||
+      !aligned(scores, 4) || !aligned(q, 4))
+    return fail(IQ_ERR_MISALIGNED, "codes, norms, qjl, rnorms must be 16-byte aligned (TMA), q and scores 4-byte");
+  if (heads > 1 && n_keys % 4 != 0)
+    return fail(IQ_ERR_MISALIGNED, "with heads > 1, n_keys must be a multiple of 4 (16-byte head strides)");
+  iq::LaunchArgs a = base_args(p, n_keys, stream);
+  a.heads = heads;
+  a.n_q = n_q;
+  a.q = q;
+  a.scores = scores;
+  a.codes_in = codes;
+  a.norms_in = norms;
+  a.qjl_in = qjl;
+  a.rnorms_in = rnorms;
+  a.qjl_img_a = p->d_qjl_a;
+  return run(iq::Kernel::kAttnScores, p, q_dtype, a);
 }
 
 iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x, uint8_t* codes,

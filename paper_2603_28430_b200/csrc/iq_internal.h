@@ -53,6 +53,7 @@ struct HostParams {
   bool has_qjl = false;
   std::vector<uint16_t> qjl_half;
   std::vector<uint8_t> qjl_img;
+  std::vector<uint8_t> qjl_img_a;   // the same S as a 128-row A operand (rows >= m zero)
 };
 
 // Sketch generator key and layout (params.cpp).
@@ -87,6 +88,14 @@ struct LaunchArgs {
   float* norms;
   const uint8_t* codes_in;
   const float* norms_in;
+  // attention consumer (k_attn_scores)
+  int heads;
+  int n_q;
+  const void* q;
+  float* scores;
+  const uint8_t* qjl_in;
+  const float* rnorms_in;
+  const uint8_t* qjl_img_a;
   double* sums;
   void* stream;
   const uint8_t* qjl_img;   // device UMMA image of S (stage 2)
@@ -94,11 +103,12 @@ struct LaunchArgs {
   float* rnorms;            // [n] residual norms (stage 2)
 };
 
-enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4 };
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5 };
 
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.
 int launch(Kernel k, int variant, int dtype, int d, int bits, const LaunchArgs& a);
+bool attn_supported(int d);   // attention consumer: d in {64, 128}
 bool gpu_supported(int d, int bits, int variant);
 
 }  // namespace iq

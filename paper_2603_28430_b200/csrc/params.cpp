@@ -332,6 +332,13 @@ bool build_qjl(HostParams* hp, std::string* err) {
       for (int k = 0; k < d; ++k)
         std::memcpy(&hp->qjl_img[umma_sw128_off(i, k, m)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
   }
+  hp->qjl_img_a.clear();
+  if (qjl_supported(d)) {
+    hp->qjl_img_a.assign(static_cast<size_t>(128) * d * 2, 0);
+    for (int i = 0; i < m; ++i)
+      for (int k = 0; k < d; ++k)
+        std::memcpy(&hp->qjl_img_a[umma_sw128_off(i, k, 128)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
+  }
   hp->has_qjl = true;
   return true;
 }
