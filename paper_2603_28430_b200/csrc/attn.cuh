@@ -46,7 +46,9 @@ struct AGeo {
   static constexpr int BAR_OFF = S_OFF + S_BYTES;
   static constexpr int SC_OFF = BAR_OFF + 256;   // per-query scales [2][NQ] floats
   static constexpr int SMEM = SC_OFF + 2 * NQ * 4 + 1024;
-  static constexpr int NWD = 4;                  // decoder / epilogue warps (TMEM lane quadrants)
+  static constexpr int NWD = 16;                 // decoder / epilogue warps (4 per TMEM lane quadrant)
+  static constexpr int GROUPS = D / 32;          // 32-coordinate groups per key
+  static_assert(TILE * GROUPS <= NWD * 32 * 2, "decode work per thread");
   static constexpr int CTA_THREADS = 32 * (NWD + 2);
   static constexpr int TMEM_COLS = 128;          // [2 buffers][stage 1, stage 2] x NQ, + NQ for S q
   static constexpr int SQ_COL = 4 * NQ;
@@ -71,6 +73,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
               const uint8_t* __restrict__ s_img, int n_q, const TQ* __restrict__ q, float* __restrict__ scores) {
   using A = AGeo<D, BITS>;
   constexpr int TILE = A::TILE, NQ = A::NQ, NWD = A::NWD, NST = A::NST, RB = A::RB, QB = A::QB;
+  constexpr int GROUPS = A::GROUPS;
   constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;
   constexpr int L = 1 << BITS;
   const bool st2 = sketch != nullptr;
@@ -112,6 +115,11 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   const uint32_t tmem = *tmem_slot;
   const int64_t tph = (n_keys + TILE - 1) / TILE;   // tiles per head
   const int64_t ntiles = tph * heads;
+  // each CTA takes a contiguous range of tiles, so it changes heads (and
+  // re-prepares its queries) about once, not on every tile
+  const int64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t_begin = blockIdx.x * per_cta;
+  const int64_t t_end = (t_begin + per_cta) < ntiles ? (t_begin + per_cta) : ntiles;
 
   if (warp == NWD) {  // ---------------------------------------------- TMA producer
     if (lane == 0) {
@@ -122,7 +130,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       }
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int64_t t = t_begin; t < t_end; t += 1) {
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
         const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
@@ -149,10 +157,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
       const uint32_t ab = smem_u32(a_base), bb = smem_u32(b_base);
       uint32_t j = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      for (int64_t t = t_begin; t < t_end; t += 1, ++j) {
         const uint32_t b = j & 1;
-        mbar_wait(&a_full[b], (j >> 1) & 1);
-        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        mbar_wait_tc(&a_full[b], (j >> 1) & 1);
+        mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll 1
         for (int part = 0; part < (st2 ? 2 : 1); ++part) {
@@ -168,7 +176,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       }
     }
   } else {  // ------------------------------------------- decoder / epilogue warps
-    const int row = 32 * warp + lane;            // key row of the tile = TMEM lane
+    // epilogue mapping: TMEM lane quadrant = warp % 4 (row = 32 quad + lane),
+    // query columns [4 part, 4 part + 4) with part = warp / 4
+    const int quad = warp & 3, part = warp >> 2;
+    const int row = 32 * quad + lane;
     const float ctab = cb.cent[lane & (L - 1)];  // C[l] in lane l of each group of L
     // +-1 fp16 pairs for 2 sketch bits (bit set = +1, R22): lane l holds the
     // half2 for bits (l & 3)
@@ -180,17 +191,22 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     uint32_t nprep = 0;                          // query preparations so far (sq_bar parity)
     auto load_queries = [&](int64_t h) {
       const TQ* qh = q + h * (int64_t)n_q * D;
-      if (threadIdx.x < NQ) {
-        const int jq = threadIdx.x;
-        float ss = 0.0f;
-        if (jq < n_q)
-          for (int i = 0; i < D; ++i) { const float v = (float)qh[jq * D + i]; ss = fmaf(v, v, ss); }
-        // sigma = 2^(8 - ceil(log2 ||q||)): |T q| <= ||q|| -> |sigma T q| <= 256;
-        // the stage-2 tile holds S sigma q / 8 (|.| <~ 4 sqrt(d) 256 / 8)
-        int e = 0;
-        frexpf(sqrtf(ss), &e);
-        qscale[jq] = ldexpf(1.0f, e - 8);                 // 1 / sigma
-        qscale[NQ + jq] = ldexpf(1.0f, e - 5);            // 8 / sigma
+      {  // per-query norms: warp w sums queries w, w + NWD, ... (lanes stride d)
+        for (int jq = warp; jq < NQ; jq += NWD) {
+          float ss = 0.0f;
+          if (jq < n_q)
+            for (int i = lane; i < D; i += 32) { const float v = (float)qh[jq * D + i]; ss = fmaf(v, v, ss); }
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+          if (lane == 0) {
+            // sigma = 2^(8 - ceil(log2 ||q||)): |T q| <= ||q|| -> |sigma T q| <= 256;
+            // the stage-2 tile holds S sigma q / 8 (|.| <~ 4 sqrt(d) 256 / 8)
+            int e = 0;
+            frexpf(sqrtf(ss), &e);
+            qscale[jq] = ldexpf(1.0f, e - 8);                 // 1 / sigma
+            qscale[NQ + jq] = ldexpf(1.0f, e - 5);            // 8 / sigma
+          }
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
       // stage 1: thread handles (query jq, block b)
@@ -224,7 +240,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         fence_async_smem();
         asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
         if (threadIdx.x == 0) {
-          mbar_wait(s_bar, 0);
+          mbar_wait_tc(s_bar, 0);
           tc_fence_after();
           const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
           const uint32_t sa = smem_u32(smem + A::S_OFF), qb = smem_u32(smem + A::QT_OFF);
@@ -234,19 +250,21 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
                      umma_desc_sw128(qb + umma_kstep_off(s, NQ)), idesc, s != 0);
           umma_commit(sq_bar);
         }
-        mbar_wait(sq_bar, nprep & 1);
+        mbar_wait_tc(sq_bar, nprep & 1);
         tc_fence_after();
-        uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + A::SQ_COL, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        const int i = 32 * warp + lane;
-        if (i < D) {
+        if (warp < 4) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + A::SQ_COL, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const int i = 32 * warp + lane;
+          if (i < D) {
 #pragma unroll
           for (int jq = 0; jq < NQ; ++jq)
-            *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
-                __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
+              *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
+                  __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
+          }
         }
+        tc_fence_before();
       }
       ++nprep;
       fence_async_smem();
@@ -255,12 +273,17 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
 
     auto epilogue = [&](uint32_t jj, int64_t tt, float rho, float gam) {
       const uint32_t b = jj & 1;
-      mbar_wait(&acc_full[b], (jj >> 1) & 1);
+      mbar_wait_tc(&acc_full[b], (jj >> 1) & 1);
       tc_fence_after();
-      uint32_t v1[16], v2[16];
-      const uint32_t lanes = (uint32_t)(32 * warp) << 16;
-      tmem_ld16(tmem + lanes + (2 * b) * NQ, v1);
-      if (st2) tmem_ld16(tmem + lanes + (2 * b + 1) * NQ, v2);
+      uint32_t v1[4], v2[4] = {0u, 0u, 0u, 0u};
+      const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16) + 4 * part;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3])
+                   : "r"(ta + (2 * b) * NQ));
+      if (st2)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3])
+                     : "r"(ta + (2 * b + 1) * NQ));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -269,10 +292,11 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       if (k < n_keys) {
         float* out = scores + h * (int64_t)n_q * n_keys + k;
 #pragma unroll
-        for (int jq = 0; jq < NQ; ++jq) {
+        for (int c = 0; c < 4; ++c) {
+          const int jq = 4 * part + c;
           if (jq < n_q) {
-            float sv = __uint_as_float(v1[jq]) * qscale[jq] * rho;
-            if (st2) sv = fmaf(__uint_as_float(v2[jq]) * qscale[NQ + jq], cpi * gam, sv);
+            float sv = __uint_as_float(v1[c]) * qscale[jq] * rho;
+            if (st2) sv = fmaf(__uint_as_float(v2[c]) * qscale[NQ + jq], cpi * gam, sv);
             out[(int64_t)jq * n_keys] = sv;
           }
         }
@@ -283,7 +307,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     uint32_t ph = 0, j = 0;
     int64_t tprev = -1, hcur = -1;
     float rho_prev = 0.0f, gam_prev = 0.0f;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    for (int64_t t = t_begin; t < t_end; t += 1, ++j) {
       const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
       if (h != hcur) {               // drain the MMAs that read the previous head's queries
         if (tprev >= 0) { epilogue(j - 1, tprev, rho_prev, gam_prev); tprev = -1; }
@@ -295,64 +319,81 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const int ss_ = s;
       if (++s == NST) { s = 0; ph ^= 1; }
       const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
-      const bool valid = row < nk;
-      const int64_t grow = h * n_keys + k0 + row;
+      const int64_t hrow0 = h * n_keys + k0;
       const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
       const uint32_t qb16 = (uint32_t)(nk * QB) & ~15u;
-      // this key's code words, norm, sketch words and gamma (smem, or global for a ragged tail)
-      uint32_t cw[RB / 4];
+      // the epilogue's row: norm and residual norm (kept in registers until the
+      // accumulator of this tile is read, one tile later)
+      const bool rvalid = row < nk;
+      const float rho = !rvalid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::N_OFF + row * 4)
+                                                                           : __ldg(norms + hrow0 + row);
+      const float gam = (!st2 || !rvalid) ? 0.0f
+                        : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::G_OFF + row * 4) : __ldg(gammas + hrow0 + row);
+      // decode mapping: thread g -> (key gr = g / GROUPS, group gs = g % GROUPS)
+      // of 32 coordinates: BITS code words and one sketch word, contiguous in
+      // the stage (consecutive lanes read consecutive words: no bank conflicts)
+      constexpr int NG = TILE * GROUPS / (NWD * 32) > 0 ? TILE * GROUPS / (NWD * 32) : 1;
+      uint32_t cw[NG][BITS], sw[NG];
+      bool gv[NG];
+      float dep = rho + gam;
 #pragma unroll
-      for (int i = 0; i < RB / 4; ++i)
-        cw[i] = !valid ? 0u
-                : ((uint32_t)(row * RB + 4 * i + 4) <= cb16) ? lds32(stg + A::C_OFF + row * RB + 4 * i)
-                                                             : __ldg(reinterpret_cast<const uint32_t*>(codes + grow * RB) + i);
-      float rho = !valid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::N_OFF + row * 4) : __ldg(norms + grow);
-      uint32_t qw[QB / 4];
-      float gam = 0.0f;
-      if (st2) {
+      for (int gi = 0; gi < NG; ++gi) {
+        const int g = threadIdx.x + gi * NWD * 32;
+        const int gr = g / GROUPS, gs = g % GROUPS;
+        gv[gi] = g < TILE * GROUPS && gr < nk;
 #pragma unroll
-        for (int i = 0; i < QB / 4; ++i)
-          qw[i] = !valid ? 0u
-                  : ((uint32_t)(row * QB + 4 * i + 4) <= qb16) ? lds32(stg + A::Q_OFF + row * QB + 4 * i)
-                                                               : __ldg(reinterpret_cast<const uint32_t*>(sketch + grow * QB) + i);
-        gam = !valid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::G_OFF + row * 4) : __ldg(gammas + grow);
+        for (int i = 0; i < BITS; ++i) {
+          const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
+          cw[gi][i] = !gv[gi] ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
+                                                        : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
+          dep += __uint_as_float(cw[gi][i] & 0x007FFFFFu);
+        }
+        if (st2) {
+          const uint32_t off = (uint32_t)(gr * QB + gs * 4);
+          sw[gi] = !gv[gi] ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
+                                                     : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
+          dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
+        }
       }
-      {
-        float dep = rho + gam;
-#pragma unroll
-        for (int i = 0; i < RB / 4; ++i) dep += __uint_as_float(cw[i] & 0x007FFFFFu);
-        __syncwarp();
-        if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
       const uint32_t b = j & 1;
-      mbar_wait(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
+      mbar_wait_tc(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
       uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
       uint8_t* a2 = a1 + A::A_BYTES;
-      // stage 1: C[code] as fp16, 8 coordinates (16 bytes) at a time
 #pragma unroll
-      for (int c8 = 0; c8 < D / 8; ++c8) {
-        uint32_t hw[4];
+      for (int gi = 0; gi < NG; ++gi) {
+        const int g = threadIdx.x + gi * NWD * 32;
+        if (g >= TILE * GROUPS) continue;
+        const int gr = g / GROUPS, gs = g % GROUPS;
+        // stage 1: C[code] as fp16 for the group's 32 coordinates, 8 per STS
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int b0 = (c8 * 8 + e) * BITS, b1 = b0 + BITS;
-          const uint32_t s0 = (b0 % 32 + BITS <= 32) ? (cw[b0 / 32] >> (b0 % 32))
-                                                     : __funnelshift_r(cw[b0 / 32], cw[b0 / 32 + 1], b0 % 32);
-          const uint32_t s1 = (b1 % 32 + BITS <= 32) ? (cw[b1 / 32] >> (b1 % 32))
-                                                     : __funnelshift_r(cw[b1 / 32], cw[b1 / 32 + 1], b1 % 32);
-          const float v0 = __shfl_sync(kFull, ctab, (int)s0, L), v1 = __shfl_sync(kFull, ctab, (int)s1, L);
-          const __half2 hh = __floats2half2_rn(v0, v1);
-          hw[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
-        }
-        *reinterpret_cast<uint4*>(a1 + umma_sw128_off(row, c8 * 8, TILE)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      }
-      if (st2) {  // stage 2: +-1 from the sketch bits, 8 at a time
-#pragma unroll
-        for (int c8 = 0; c8 < D / 8; ++c8) {
-          const uint32_t byte = qw[c8 / 4] >> ((c8 % 4) * 8);
+        for (int c8 = 0; c8 < 4; ++c8) {
           uint32_t hw[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__shfl_sync(kFull, (int)ptab, (int)(byte >> (2 * e)), 4);
-          *reinterpret_cast<uint4*>(a2 + umma_sw128_off(row, c8 * 8, TILE)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          for (int e = 0; e < 8; e += 2) {
+            const int b0 = (c8 * 8 + e) * BITS, b1 = b0 + BITS;
+            const uint32_t s0 = (b0 % 32 + BITS <= 32) ? (cw[gi][b0 / 32] >> (b0 % 32))
+                                                       : __funnelshift_r(cw[gi][b0 / 32], cw[gi][b0 / 32 + 1], b0 % 32);
+            const uint32_t s1 = (b1 % 32 + BITS <= 32) ? (cw[gi][b1 / 32] >> (b1 % 32))
+                                                       : __funnelshift_r(cw[gi][b1 / 32], cw[gi][b1 / 32 + 1], b1 % 32);
+            const float v0 = __shfl_sync(kFull, ctab, (int)s0, L), v1 = __shfl_sync(kFull, ctab, (int)s1, L);
+            const __half2 hh = __floats2half2_rn(v0, v1);
+            hw[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+          }
+          *reinterpret_cast<uint4*>(a1 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
+              make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        }
+        if (st2) {  // stage 2: +-1 from the sketch bits
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            const uint32_t byte = sw[gi] >> (c8 * 8);
+            uint32_t hw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__shfl_sync(kFull, (int)ptab, (int)(byte >> (2 * e)), 4);
+            *reinterpret_cast<uint4*>(a2 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
+                make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          }
         }
       }
       fence_async_smem();

@@ -193,6 +193,32 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait without a suspend-time hint (the hardware's default bounded wait):
+// used for barriers completed by tcgen05.commit, whose waiters otherwise sit
+// out the full suspend hint
+__device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+#ifndef IQ_TC_SPIN
+#define IQ_TC_SPIN 1
+#endif
+__device__ __forceinline__ void mbar_wait_tc(uint64_t* bar, uint32_t parity) {
+#if IQ_TC_SPIN
+  while (!mbar_try_wait_nohint(bar, parity)) {
+  }
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
+}
 // Blocking wait.  The retry loop is C++ (compiler-visible), so the compiler
 // places the warp's reconvergence point (BSSY/BSYNC) right after it, before
 // the shared loads and shuffles that follow.

@@ -211,12 +211,12 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
       // D[128 x M] (+)= A[128 x D] * S[M x D]^T: fp16 inputs, fp32 accumulate
       const uint32_t idesc = (1u << 4) | ((uint32_t)(M >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
       const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), sb = smem_u32(s_sm);
-      mbar_wait(s_bar, 0);
+      mbar_wait_tc(s_bar, 0);
       uint32_t j = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
         const uint32_t b = j & 1;
-        mbar_wait(a_full, j & 1);
-        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        mbar_wait_tc(a_full, j & 1);
+        mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t td = tmem + b * M;
 #pragma unroll
@@ -254,7 +254,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
 
     auto epilogue = [&](uint32_t jj, int64_t tt) {
       const uint32_t b = jj & 1;
-      mbar_wait(&acc_full[b], (jj >> 1) & 1);
+      mbar_wait_tc(&acc_full[b], (jj >> 1) & 1);
       tc_fence_after();
       const int row = 32 * quad + lane;
       const int64_t v = tt * TILE + row;
@@ -395,7 +395,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         const float2 sr = mul2(rinv, bc(256.0f));
         // the previous tile's MMAs must have consumed the A tiles (the
         // stage-1 work above overlaps them)
-        if (u == 0) mbar_wait(a_free, (j & 1) ^ 1);
+        if (u == 0) mbar_wait_tc(a_free, (j & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           float ta[EPC], tb[EPC];

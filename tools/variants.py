@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "qjl8": ["-DIQ_QJL_NWC=8"],
+    "tchint": ["-DIQ_TC_SPIN=0"],
 }
 
 
