@@ -9,15 +9,23 @@
 //   s[h][j][k] = <q_hj, x^_hk> = rho_hk <T q_hj, C[code_hk]>        (T orthogonal)
 //              + sqrt(pi/2)/m gamma_hk <S q_hj, sign_hk>            (stage 2, optional)
 // so no key is ever inverse-rotated: the queries are rotated once per head
-// and the keys only decoded.  Per 128-key tile:
-//   decoder warps (4, thread = key row) : TMA-staged codes (+ sketch bits)
-//       -> C[code] as fp16 (width-L shuffle table) and +-1 fp16 from the
-//       sketch bits (width-4 shuffle table of half2 pairs), written to
-//       K-major 128B-swizzled UMMA A tiles;
-//   MMA warp (one elected thread)       : tcgen05.mma kind::f16, M = 128 keys,
-//       N = 16 query slots, K = d, into TMEM (stage-1 and stage-2 accumulators);
-//   decoder warps, one tile later       : tcgen05.ld, scale by rho_k / sigma_j
-//       (+ gamma_k sqrt(pi/2)/m / tau_j), store s[h][j][k] (coalesced in k).
+// and the keys only decoded.  Warp roles of the persistent CTA (one per SM,
+// each owning a contiguous range of 128-key tiles):
+//   TMA producer (1 lane) : codes, norms (+ sketch bits, gammas) of a tile
+//                           into a deep ring of small stages;
+//   16 decoder warps      : C[code] as fp16 (width-L shuffle table) and +-1
+//                           fp16 from the sketch bits (width-4 shuffle table
+//                           of half2 pairs) into K-major 128B-swizzled UMMA A
+//                           tiles (double-buffered), plus a per-buffer side
+//                           table (rho, gamma, the head's query scales);
+//   MMA issuer (1 lane)   : tcgen05.mma kind::f16, M = 128 keys, N = 16 query
+//                           slots, K = d, into TMEM (stage-1 and stage-2
+//                           accumulators, double-buffered);
+//   4 epilogue warps      : tcgen05.ld (thread = key), scale, store
+//                           s[h][j][k] (coalesced in k).
+// At a head change the decoders drain the MMAs, rotate the new queries on
+// the CUDA cores (T q: 16 FMA per block) and compute S q on the tensor cores
+// (S staged through the drained A buffers).
 #pragma once
 #include "qjl.cuh"
 
@@ -34,35 +42,40 @@ struct AGeo {
   static constexpr int N_OFF = (TILE * RB + 15) / 16 * 16;
   static constexpr int Q_OFF = N_OFF + TILE * 4;
   static constexpr int G_OFF = Q_OFF + TILE * QB;
-  static constexpr int STAGE = (G_OFF + TILE * 4 + 1023) / 1024 * 1024;
-  static constexpr int NST = 3;
+  static constexpr int STAGE = (G_OFF + TILE * 4 + 127) / 128 * 128;
   static constexpr int A_BYTES = TILE * D * 2;   // one fp16 A tile
   static constexpr int B_BYTES = NQ * D * 2;     // one fp16 B tile (queries)
-  static constexpr int A_OFF = NST * STAGE;      // [2 buffers][stage 1, stage 2]
+  static constexpr int S_BYTES = 128 * D * 2;    // S as a 128-row A operand (staged in the A buffers)
+  static constexpr int A_OFF = 0;                // [2 buffers][stage 1, stage 2]
   static constexpr int B_OFF = A_OFF + 4 * A_BYTES;
   static constexpr int QT_OFF = B_OFF + 2 * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
-  static constexpr int S_OFF = QT_OFF + B_BYTES;        // S image, 128 rows (A of the S q MMA)
-  static constexpr int S_BYTES = 128 * D * 2;
-  static constexpr int BAR_OFF = S_OFF + S_BYTES;
-  static constexpr int SC_OFF = BAR_OFF + 256;   // per-query scales [2][NQ] floats
-  static constexpr int SMEM = SC_OFF + 2 * NQ * 4 + 1024;
-  static constexpr int NWD = 16;                 // decoder / epilogue warps (4 per TMEM lane quadrant)
+  static constexpr int SIDE_OFF = QT_OFF + B_BYTES;    // per buffer: rho[128], gamma[128], scales[2][16]
+  static constexpr int SIDE_BYTES = (2 * TILE + 2 * NQ) * 4;
+  static constexpr int QS_OFF = SIDE_OFF + 2 * SIDE_BYTES;   // the current head's scales [2][16]
+  static constexpr int BAR_OFF = QS_OFF + 2 * NQ * 4;
+  static constexpr int RING_OFF = (BAR_OFF + 512 + 127) / 128 * 128;
+  static constexpr int RING_MAX = 227 * 1024 - RING_OFF - 1024;
+  static constexpr int NST = (RING_MAX / STAGE) < 16 ? (RING_MAX / STAGE) : 16;
+  static constexpr int SMEM = RING_OFF + NST * STAGE + 1024;
+  static constexpr int NWD = 16;                 // decoder warps
+  static constexpr int NWE = 4;                  // epilogue warps (one per TMEM lane quadrant)
+  static constexpr int W_PROD = NWD + NWE, W_MMA = NWD + NWE + 1;
+  static constexpr int CTA_THREADS = 32 * (NWD + NWE + 2);
   static constexpr int GROUPS = D / 32;          // 32-coordinate groups per key
-  static_assert(TILE * GROUPS <= NWD * 32 * 2, "decode work per thread");
-  static constexpr int CTA_THREADS = 32 * (NWD + 2);
   static constexpr int TMEM_COLS = 128;          // [2 buffers][stage 1, stage 2] x NQ, + NQ for S q
   static constexpr int SQ_COL = 4 * NQ;
   static_assert(D == 64 || D == 128, "attention consumer: d in {64, 128}");
+  static_assert(NST >= 3, "ring too shallow");
+  static_assert(S_BYTES <= 4 * A_BYTES, "S staging");
 };
 
-__device__ __forceinline__ uint32_t tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
         "=r"(v[15])
       : "r"(taddr));
-  return 0;
 }
 
 template <class TQ, int D, int BITS, int VAR>
@@ -82,29 +95,30 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* a_base = smem + A::A_OFF;            // A[buf][part] at a_base + (2 buf + part) A_BYTES
   uint8_t* b_base = smem + A::B_OFF;            // B[part]
-  float* qscale = reinterpret_cast<float*>(smem + A::SC_OFF);   // [2][NQ]: 1/sigma_j, 1/tau_j
+  float* qs = reinterpret_cast<float*>(smem + A::QS_OFF);   // [2][NQ]: 1/sigma_j, 8/sigma_j
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
   uint64_t* empty = full + NST;
-  uint64_t* a_full = empty + NST;    // [2]
-  uint64_t* a_free = a_full + 2;     // [2]
-  uint64_t* acc_full = a_free + 2;   // [2]
-  uint64_t* acc_empty = acc_full + 2;  // [2]
-  uint64_t* s_bar = acc_empty + 2;     // S image loaded
+  uint64_t* a_full = empty + NST;      // [2] decoders -> MMA
+  uint64_t* a_free = a_full + 2;       // [2] MMA -> decoders (A buffer consumed)
+  uint64_t* acc_full = a_free + 2;     // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;  // [2] epilogue -> MMA, decoders (accumulator and side table free)
+  uint64_t* s_bar = acc_empty + 2;     // S image staged (per head change)
   uint64_t* sq_bar = s_bar + 1;        // S q MMA done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_bar + 1);
+  uint8_t* ring = smem + A::RING_OFF;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWD); }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1);
-      mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], NWD);
+      mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], A::NWE);
     }
     mbar_init(s_bar, 1);
     mbar_init(sq_bar, 1);
     fence_mbar_init();
   }
-  if (warp == NWD + 1) {
+  if (warp == A::W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(A::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -121,16 +135,12 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   const int64_t t_begin = blockIdx.x * per_cta;
   const int64_t t_end = (t_begin + per_cta) < ntiles ? (t_begin + per_cta) : ntiles;
 
-  if (warp == NWD) {  // ---------------------------------------------- TMA producer
+  if (warp == A::W_PROD) {  // ---------------------------------------- TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      if (st2) {
-        mbar_arrive_expect_tx(s_bar, A::S_BYTES);
-        bulk_g2s(smem + A::S_OFF, s_img, A::S_BYTES, s_bar, policy_evict_last());
-      }
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = t_begin; t < t_end; t += 1) {
+      for (int64_t t = t_begin; t < t_end; ++t) {
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
         const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
@@ -139,7 +149,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
         const uint32_t qb16 = st2 ? ((uint32_t)(nk * QB) & ~15u) : 0u, gb16 = st2 ? nb16 : 0u;
         const uint32_t tot = cb16 + nb16 + qb16 + gb16;
-        uint8_t* stg = smem + s * A::STAGE;
+        uint8_t* stg = ring + s * A::STAGE;
         if (tot == 0) {
           mbar_arrive(&full[s]);
         } else {
@@ -152,12 +162,12 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         if (++s == NST) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == NWD + 1) {  // ------------------------------------------ MMA issuer
+  } else if (warp == A::W_MMA) {  // ------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
       const uint32_t ab = smem_u32(a_base), bb = smem_u32(b_base);
       uint32_t j = 0;
-      for (int64_t t = t_begin; t < t_end; t += 1, ++j) {
+      for (int64_t t = t_begin; t < t_end; ++t, ++j) {
         const uint32_t b = j & 1;
         mbar_wait_tc(&a_full[b], (j >> 1) & 1);
         mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);
@@ -175,37 +185,67 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         umma_commit(&acc_full[b]);
       }
     }
-  } else {  // ------------------------------------------- decoder / epilogue warps
-    // epilogue mapping: TMEM lane quadrant = warp % 4 (row = 32 quad + lane),
-    // query columns [4 part, 4 part + 4) with part = warp / 4
-    const int quad = warp & 3, part = warp >> 2;
+  } else if (warp >= NWD) {  // --------------------------------------------- epilogue
+    const int quad = warp & 3;                   // TMEM lane quadrant (warp id % 4)
     const int row = 32 * quad + lane;
+    const float cpi = 1.2533141373155003f / (float)D;   // sqrt(pi/2) / m, m = d (R20)
+    uint32_t j = 0;
+    for (int64_t t = t_begin; t < t_end; ++t, ++j) {
+      const uint32_t b = j & 1;
+      mbar_wait_tc(&acc_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v1[16], v2[16];
+      const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16);
+      tmem_ld16(ta + (2 * b) * NQ, v1);
+      if (st2) tmem_ld16(ta + (2 * b + 1) * NQ, v2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + b * A::SIDE_BYTES);
+      const int64_t h = t / tph, k = (t - h * tph) * TILE + row;
+      if (k < n_keys) {
+        const float rho = side[row], gam = side[TILE + row];
+        float* out = scores + h * (int64_t)n_q * n_keys + k;
+#pragma unroll
+        for (int jq = 0; jq < NQ; ++jq) {
+          if (jq < n_q) {
+            float sv = __uint_as_float(v1[jq]) * side[2 * TILE + jq] * rho;
+            if (st2) sv = fmaf(__uint_as_float(v2[jq]) * side[2 * TILE + NQ + jq], cpi * gam, sv);
+            __stcs(out + (int64_t)jq * n_keys, sv);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);   // accumulator and side table b are free
+    }
+  } else {  // ------------------------------------------------------------- decoders
     const float ctab = cb.cent[lane & (L - 1)];  // C[l] in lane l of each group of L
     // +-1 fp16 pairs for 2 sketch bits (bit set = +1, R22): lane l holds the
     // half2 for bits (l & 3)
     const uint32_t ptab = ((lane & 1) ? 0x3C00u : 0xBC00u) | ((lane & 2) ? 0x3C000000u : 0xBC000000u);
-    const float cpi = 1.2533141373155003f / (float)D;   // sqrt(pi/2) / m, m = d (R20)
+    uint32_t nprep = 0;                          // query preparations so far (s_bar / sq_bar parity)
 
     // rotate the head's queries into the B tiles: q' = T q (stage 1) and
     // S q (stage 2), fp16 with per-query power-of-two scales
-    uint32_t nprep = 0;                          // query preparations so far (sq_bar parity)
     auto load_queries = [&](int64_t h) {
       const TQ* qh = q + h * (int64_t)n_q * D;
-      {  // per-query norms: warp w sums queries w, w + NWD, ... (lanes stride d)
-        for (int jq = warp; jq < NQ; jq += NWD) {
-          float ss = 0.0f;
-          if (jq < n_q)
-            for (int i = lane; i < D; i += 32) { const float v = (float)qh[jq * D + i]; ss = fmaf(v, v, ss); }
+      if (st2 && threadIdx.x == 0) {             // stage S in the drained A buffers
+        mbar_arrive_expect_tx(s_bar, A::S_BYTES);
+        bulk_g2s(a_base, s_img, A::S_BYTES, s_bar, policy_evict_last());
+      }
+      // per-query norms: warp w sums query w (lanes stride d)
+      for (int jq = warp; jq < NQ; jq += NWD) {
+        float ss = 0.0f;
+        if (jq < n_q)
+          for (int i = lane; i < D; i += 32) { const float v = (float)qh[jq * D + i]; ss = fmaf(v, v, ss); }
 #pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
-          if (lane == 0) {
-            // sigma = 2^(8 - ceil(log2 ||q||)): |T q| <= ||q|| -> |sigma T q| <= 256;
-            // the stage-2 tile holds S sigma q / 8 (|.| <~ 4 sqrt(d) 256 / 8)
-            int e = 0;
-            frexpf(sqrtf(ss), &e);
-            qscale[jq] = ldexpf(1.0f, e - 8);                 // 1 / sigma
-            qscale[NQ + jq] = ldexpf(1.0f, e - 5);            // 8 / sigma
-          }
+        for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+        if (lane == 0) {
+          // sigma = 2^(8 - ceil(log2 ||q||)): |T q| <= ||q|| -> |sigma T q| <= 256;
+          // the stage-2 tile holds S sigma q / 8 (|.| <~ 4 sqrt(d) 256 / 8)
+          int e = 0;
+          frexpf(sqrtf(ss), &e);
+          qs[jq] = ldexpf(1.0f, e - 8);                 // 1 / sigma
+          qs[NQ + jq] = ldexpf(1.0f, e - 5);            // 8 / sigma
         }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
@@ -213,7 +253,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       for (int w = threadIdx.x; w < NQ * (D / PW); w += NWD * 32) {
         const int jq = w / (D / PW), b = w % (D / PW);
         float xv[PW], yv[PW];
-        const float sg = 1.0f / qscale[jq];
+        const float sg = 1.0f / qs[jq];
 #pragma unroll
         for (int c = 0; c < PW; ++c) xv[c] = jq < n_q ? (float)qh[jq * D + b * PW + c] * sg : 0.0f;
 #pragma unroll
@@ -230,20 +270,20 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       if (st2) {
         // stage 2: S q on the tensor cores.  B = sigma q as fp16 (queries x d),
         // A = S (128 x d, rows >= m zero), D = S (sigma q)^T in TMEM; thread i
-        // then holds (S sigma q_j)_i for the 16 query slots and writes
-        // (S sigma q_j)_i / 8 into the stage-2 B tile (row j, column i)
+        // of warps 0..3 then holds (S sigma q_j)_i for the 16 query slots and
+        // writes (S sigma q_j)_i / 8 into the stage-2 B tile (row j, column i)
         for (int w = threadIdx.x; w < NQ * D; w += NWD * 32) {
           const int jq = w / D, k = w % D;
-          const float v = jq < n_q ? (float)qh[jq * D + k] / qscale[jq] : 0.0f;
+          const float v = jq < n_q ? (float)qh[jq * D + k] / qs[jq] : 0.0f;
           *reinterpret_cast<__half*>(smem + A::QT_OFF + umma_sw128_off(jq, k, NQ)) = __float2half_rn(v);
         }
         fence_async_smem();
         asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
         if (threadIdx.x == 0) {
-          mbar_wait_tc(s_bar, 0);
+          mbar_wait_tc(s_bar, nprep & 1);
           tc_fence_after();
           const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-          const uint32_t sa = smem_u32(smem + A::S_OFF), qb = smem_u32(smem + A::QT_OFF);
+          const uint32_t sa = smem_u32(a_base), qb = smem_u32(smem + A::QT_OFF);
 #pragma unroll
           for (int s = 0; s < D / 16; ++s)
             umma_f16(tmem + A::SQ_COL, umma_desc_sw128(sa + umma_kstep_off(s, 128)),
@@ -259,7 +299,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
           const int i = 32 * warp + lane;
           if (i < D) {
 #pragma unroll
-          for (int jq = 0; jq < NQ; ++jq)
+            for (int jq = 0; jq < NQ; ++jq)
               *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
                   __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
           }
@@ -268,97 +308,75 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       }
       ++nprep;
       fence_async_smem();
-      asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
-    };
-
-    auto epilogue = [&](uint32_t jj, int64_t tt, float rho, float gam) {
-      const uint32_t b = jj & 1;
-      mbar_wait_tc(&acc_full[b], (jj >> 1) & 1);
-      tc_fence_after();
-      uint32_t v1[4], v2[4] = {0u, 0u, 0u, 0u};
-      const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16) + 4 * part;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3])
-                   : "r"(ta + (2 * b) * NQ));
-      if (st2)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3])
-                     : "r"(ta + (2 * b + 1) * NQ));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
-      const int64_t h = tt / tph, k = (tt - h * tph) * TILE + row;
-      if (k < n_keys) {
-        float* out = scores + h * (int64_t)n_q * n_keys + k;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int jq = 4 * part + c;
-          if (jq < n_q) {
-            float sv = __uint_as_float(v1[c]) * qscale[jq] * rho;
-            if (st2) sv = fmaf(__uint_as_float(v2[c]) * qscale[NQ + jq], cpi * gam, sv);
-            out[(int64_t)jq * n_keys] = sv;
-          }
-        }
-      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");   // B tiles, qs and the A buffers ready
     };
 
     int s = 0;
     uint32_t ph = 0, j = 0;
-    int64_t tprev = -1, hcur = -1;
-    float rho_prev = 0.0f, gam_prev = 0.0f;
-    for (int64_t t = t_begin; t < t_end; t += 1, ++j) {
+    int64_t hcur = -1;
+    float qs_mine = 0.0f;                        // qs[threadIdx.x] of the current head (threads < 2 NQ)
+    for (int64_t t = t_begin; t < t_end; ++t, ++j) {
       const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
-      if (h != hcur) {               // drain the MMAs that read the previous head's queries
-        if (tprev >= 0) { epilogue(j - 1, tprev, rho_prev, gam_prev); tprev = -1; }
+      const uint32_t b = j & 1;
+      if (h != hcur) {
+        // drain: the last MMA issued (tile j - 1) completes after every
+        // earlier one, so the B tiles and both A buffers are free
+        if (j > 0) mbar_wait_tc(&a_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
         load_queries(h);
         hcur = h;
+        if (threadIdx.x < 2 * NQ) qs_mine = qs[threadIdx.x];
       }
       mbar_wait(&full[s], ph);
-      const uint8_t* stg = smem + s * A::STAGE;
+      const uint8_t* stg = ring + s * A::STAGE;
       const int ss_ = s;
       if (++s == NST) { s = 0; ph ^= 1; }
       const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
       const int64_t hrow0 = h * n_keys + k0;
       const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
       const uint32_t qb16 = (uint32_t)(nk * QB) & ~15u;
-      // the epilogue's row: norm and residual norm (kept in registers until the
-      // accumulator of this tile is read, one tile later)
-      const bool rvalid = row < nk;
-      const float rho = !rvalid ? 0.0f : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::N_OFF + row * 4)
-                                                                           : __ldg(norms + hrow0 + row);
-      const float gam = (!st2 || !rvalid) ? 0.0f
-                        : ((uint32_t)(row * 4 + 4) <= nb16) ? ldsf(stg + A::G_OFF + row * 4) : __ldg(gammas + hrow0 + row);
       // decode mapping: thread g -> (key gr = g / GROUPS, group gs = g % GROUPS)
       // of 32 coordinates: BITS code words and one sketch word, contiguous in
       // the stage (consecutive lanes read consecutive words: no bank conflicts)
       constexpr int NG = TILE * GROUPS / (NWD * 32) > 0 ? TILE * GROUPS / (NWD * 32) : 1;
       uint32_t cw[NG][BITS], sw[NG];
-      bool gv[NG];
-      float dep = rho + gam;
+      float dep = 0.0f;
 #pragma unroll
       for (int gi = 0; gi < NG; ++gi) {
         const int g = threadIdx.x + gi * NWD * 32;
         const int gr = g / GROUPS, gs = g % GROUPS;
-        gv[gi] = g < TILE * GROUPS && gr < nk;
+        const bool gv = g < TILE * GROUPS && gr < nk;
 #pragma unroll
         for (int i = 0; i < BITS; ++i) {
           const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
-          cw[gi][i] = !gv[gi] ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
-                                                        : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
+          cw[gi][i] = !gv ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
+                                                    : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
           dep += __uint_as_float(cw[gi][i] & 0x007FFFFFu);
         }
+        sw[gi] = 0u;
         if (st2) {
           const uint32_t off = (uint32_t)(gr * QB + gs * 4);
-          sw[gi] = !gv[gi] ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
-                                                     : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
+          sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
+                                                 : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
           dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
         }
       }
+      // rho and gamma of the tile's keys for the side table
+      float rg = 0.0f;
+      if (threadIdx.x < 2 * TILE) {
+        const int r = threadIdx.x & (TILE - 1);
+        const bool isg = threadIdx.x >= TILE;
+        if (r < nk && (!isg || st2))
+          rg = ((uint32_t)(r * 4 + 4) <= nb16) ? ldsf(stg + (isg ? A::G_OFF : A::N_OFF) + r * 4)
+                                               : __ldg((isg ? gammas : norms) + hrow0 + r);
+        dep += rg;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
-      const uint32_t b = j & 1;
       mbar_wait_tc(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
+      mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);   // side table b read by the epilogue of tile j - 2
+      float* side = reinterpret_cast<float*>(smem + A::SIDE_OFF + b * A::SIDE_BYTES);
+      if (threadIdx.x < 2 * TILE) side[threadIdx.x] = rg;
+      if (threadIdx.x < 2 * NQ) side[2 * TILE + threadIdx.x] = qs_mine;
       uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
       uint8_t* a2 = a1 + A::A_BYTES;
 #pragma unroll
@@ -399,16 +417,11 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[b]);
-      if (tprev >= 0) epilogue(j - 1, tprev, rho_prev, gam_prev);
-      tprev = t;
-      rho_prev = rho;
-      gam_prev = gam;
     }
-    if (tprev >= 0) epilogue(j - 1, tprev, rho_prev, gam_prev);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == NWD + 1) {
+  if (warp == A::W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(A::TMEM_COLS));
   }
