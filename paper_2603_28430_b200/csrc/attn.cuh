@@ -140,9 +140,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = t_begin; t < t_end; ++t) {
+      int64_t h = t_begin / tph, k0 = (t_begin - h * tph) * TILE;   // advanced incrementally
+      for (int64_t t = t_begin; t < t_end; ++t, k0 += TILE) {
+        if (k0 >= n_keys) { k0 = 0; ++h; }
         mbar_wait(&empty[s], ph ^ 1);
-        const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
         const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
         const int64_t row0 = h * n_keys + k0;
         // whole 16-byte units; a ragged remainder is read from global memory
@@ -190,7 +191,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     const int row = 32 * quad + lane;
     const float cpi = 1.2533141373155003f / (float)D;   // sqrt(pi/2) / m, m = d (R20)
     uint32_t j = 0;
-    for (int64_t t = t_begin; t < t_end; ++t, ++j) {
+    int64_t h = t_begin / tph, k0 = (t_begin - h * tph) * TILE;
+    for (int64_t t = t_begin; t < t_end; ++t, ++j, k0 += TILE) {
+      if (k0 >= n_keys) { k0 = 0; ++h; }
       const uint32_t b = j & 1;
       mbar_wait_tc(&acc_full[b], (j >> 1) & 1);
       tc_fence_after();
@@ -201,7 +204,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + b * A::SIDE_BYTES);
-      const int64_t h = t / tph, k = (t - h * tph) * TILE + row;
+      const int64_t k = k0 + row;
       if (k < n_keys) {
         const float rho = side[row], gam = side[TILE + row];
         float* out = scores + h * (int64_t)n_q * n_keys + k;
@@ -315,8 +318,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     uint32_t ph = 0, j = 0;
     int64_t hcur = -1;
     float qs_mine = 0.0f;                        // qs[threadIdx.x] of the current head (threads < 2 NQ)
-    for (int64_t t = t_begin; t < t_end; ++t, ++j) {
-      const int64_t h = t / tph, k0 = (t - h * tph) * TILE;
+    int64_t h = t_begin / tph, k0 = (t_begin - h * tph) * TILE;
+    for (int64_t t = t_begin; t < t_end; ++t, ++j, k0 += TILE) {
+      if (k0 >= n_keys) { k0 = 0; ++h; }
       const uint32_t b = j & 1;
       if (h != hcur) {
         // drain: the last MMA issued (tile j - 1) completes after every
@@ -334,6 +338,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const int64_t hrow0 = h * n_keys + k0;
       const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
       const uint32_t qb16 = (uint32_t)(nk * QB) & ~15u;
+      const bool full_tile = nk == TILE;         // TILE * (RB, 4, QB) are 16-byte multiples
       // decode mapping: thread g -> (key gr = g / GROUPS, group gs = g % GROUPS)
       // of 32 coordinates: BITS code words and one sketch word, contiguous in
       // the stage (consecutive lanes read consecutive words: no bank conflicts)
@@ -345,20 +350,27 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         const int g = threadIdx.x + gi * NWD * 32;
         const int gr = g / GROUPS, gs = g % GROUPS;
         const bool gv = g < TILE * GROUPS && gr < nk;
+        if (full_tile) {           // everything is in the stage
 #pragma unroll
-        for (int i = 0; i < BITS; ++i) {
-          const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
-          cw[gi][i] = !gv ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
-                                                    : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
-          dep += __uint_as_float(cw[gi][i] & 0x007FFFFFu);
+          for (int i = 0; i < BITS; ++i) cw[gi][i] = gv ? lds32(stg + A::C_OFF + gr * RB + (gs * BITS + i) * 4) : 0u;
+          sw[gi] = (st2 && gv) ? lds32(stg + A::Q_OFF + gr * QB + gs * 4) : 0u;
+        } else {
+#pragma unroll
+          for (int i = 0; i < BITS; ++i) {
+            const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
+            cw[gi][i] = !gv ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
+                                                      : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
+          }
+          sw[gi] = 0u;
+          if (st2) {
+            const uint32_t off = (uint32_t)(gr * QB + gs * 4);
+            sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
+                                                   : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
+          }
         }
-        sw[gi] = 0u;
-        if (st2) {
-          const uint32_t off = (uint32_t)(gr * QB + gs * 4);
-          sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
-                                                 : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
-          dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
-        }
+#pragma unroll
+        for (int i = 0; i < BITS; ++i) dep += __uint_as_float(cw[gi][i] & 0x007FFFFFu);
+        dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
       }
       // rho and gamma of the tile's keys for the side table
       float rg = 0.0f;
@@ -366,8 +378,8 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         const int r = threadIdx.x & (TILE - 1);
         const bool isg = threadIdx.x >= TILE;
         if (r < nk && (!isg || st2))
-          rg = ((uint32_t)(r * 4 + 4) <= nb16) ? ldsf(stg + (isg ? A::G_OFF : A::N_OFF) + r * 4)
-                                               : __ldg((isg ? gammas : norms) + hrow0 + r);
+          rg = (full_tile || (uint32_t)(r * 4 + 4) <= nb16) ? ldsf(stg + (isg ? A::G_OFF : A::N_OFF) + r * 4)
+                                                            : __ldg((isg ? gammas : norms) + hrow0 + r);
         dep += rg;
       }
       __syncwarp();
