@@ -371,6 +371,20 @@ def main():
                                     "bytes_per_launch": b, "vectors_per_s": a.n / (t / 1e3),
                                     "tensor_tflops": a.n * 4 * a.d * a.d / (t / 1e3) / 1e12}
             del qj, rn
+        if a.d in (64, 128):   # fused KV-cache decode consumer (NEXT row 2), on this batch as keys
+            H = 32                                  # heads of n/32 keys each, 4 queries per head (GQA)
+            nk = a.n // H
+            qh = torch.randn((H, 4, a.d), dtype=tdt, device=dev)
+            sc = torch.empty((H, 4, nk), dtype=torch.float32, device=dev)
+            c3, n3 = codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk)
+            iq.iq_quantize(p, xs[0][:H * nk], codes[:H * nk], norms[:H * nk], stream=stream)
+            t = time_launches(torch, lambda i: iq.iq_attention_scores(p, c3, n3, qh, scores=sc, stream=stream),
+                              max(10, a.steps), 3, stream)
+            b = H * nk * (p.code_bytes + 4 + 4 * 4)
+            kern["attention_scores"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                                        "bytes_per_launch": b, "keys_per_s": H * nk / (t / 1e3),
+                                        "shape": f"{H} heads x {nk} keys, 4 queries per head, stage 1"}
+            del qh, sc
         out["kernels"] = kern
         del codes, norms
 
