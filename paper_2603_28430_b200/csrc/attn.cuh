@@ -52,7 +52,13 @@ struct AGeo {
   static constexpr int SIDE_OFF = QT_OFF + B_BYTES;    // per buffer: rho[128], gamma[128], scales[2][16]
   static constexpr int SIDE_BYTES = (2 * TILE + 2 * NQ) * 4;
   static constexpr int QS_OFF = SIDE_OFF + 2 * SIDE_BYTES;   // the current head's scales [2][16]
-  static constexpr int BAR_OFF = QS_OFF + 2 * NQ * 4;
+  // lookup tables replicated across the 32 banks (entry e of lane l at
+  // e * stride + 4 l, so every lane reads its own bank): a code PAIR -> half2
+  // (C[c0], C[c1]), and 4 sketch bits -> 4 halves of +-1 (two words)
+  static constexpr int PAIRS = 1 << (2 * BITS);
+  static constexpr int PT_OFF = QS_OFF + 2 * NQ * 4;
+  static constexpr int ST_OFF = PT_OFF + PAIRS * 128;
+  static constexpr int BAR_OFF = ST_OFF + 16 * 256;
   static constexpr int RING_OFF = (BAR_OFF + 512 + 127) / 128 * 128;
   static constexpr int RING_MAX = 227 * 1024 - RING_OFF - 1024;
   static constexpr int NST = (RING_MAX / STAGE) < 16 ? (RING_MAX / STAGE) : 16;
@@ -221,10 +227,25 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       if (lane == 0) mbar_arrive(&acc_empty[b]);   // accumulator and side table b are free
     }
   } else {  // ------------------------------------------------------------- decoders
-    const float ctab = cb.cent[lane & (L - 1)];  // C[l] in lane l of each group of L
-    // +-1 fp16 pairs for 2 sketch bits (bit set = +1, R22): lane l holds the
-    // half2 for bits (l & 3)
-    const uint32_t ptab = ((lane & 1) ? 0x3C00u : 0xBC00u) | ((lane & 2) ? 0x3C000000u : 0xBC000000u);
+    // build the replicated lookup tables (once per CTA)
+    for (int e = threadIdx.x; e < A::PAIRS * 32; e += NWD * 32) {
+      const int pr = e >> 5, l = e & 31;
+      const __half2 hv = __floats2half2_rn(cb.cent[pr & (L - 1)], cb.cent[pr >> BITS]);
+      *reinterpret_cast<__half2*>(smem + A::PT_OFF + pr * 128 + 4 * l) = hv;
+    }
+    for (int e = threadIdx.x; e < 16 * 32; e += NWD * 32) {   // bit set = +1 (R22)
+      const int nib = e >> 5, l = e & 31;
+      uint32_t w[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        w[k] = ((nib >> (2 * k)) & 1 ? 0x3C00u : 0xBC00u) | ((nib >> (2 * k + 1)) & 1 ? 0x3C000000u : 0xBC000000u);
+      *reinterpret_cast<uint2*>(smem + A::ST_OFF + nib * 256 + 8 * l) = make_uint2(w[0], w[1]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");
+    // table address = (index * stride | lane offset) + base: the OR needs the
+    // lane offset below the stride; the (warp-uniform) base is added after
+    const uint32_t pt_base = smem_u32(smem + A::PT_OFF), st_base = smem_u32(smem + A::ST_OFF);
+    const uint32_t pt_lane = 4 * lane, st_lane = 8 * lane;
     uint32_t nprep = 0;                          // query preparations so far (s_bar / sq_bar parity)
 
     // rotate the head's queries into the B tiles: q' = T q (stage 1) and
@@ -396,31 +417,40 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         const int g = threadIdx.x + gi * NWD * 32;
         if (g >= TILE * GROUPS) continue;
         const int gr = g / GROUPS, gs = g % GROUPS;
-        // stage 1: C[code] as fp16 for the group's 32 coordinates, 8 per STS
+        // stage 1: C[code] as fp16, two coordinates per lookup: the pair's
+        // 2 BITS-bit field is shifted to bit 7 and OR-ed into this lane's
+        // column of the pair table (one SHF + LOP3 + LDS per pair)
 #pragma unroll
         for (int c8 = 0; c8 < 4; ++c8) {
           uint32_t hw[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            const int b0 = (c8 * 8 + e) * BITS, b1 = b0 + BITS;
-            const uint32_t s0 = (b0 % 32 + BITS <= 32) ? (cw[gi][b0 / 32] >> (b0 % 32))
-                                                       : __funnelshift_r(cw[gi][b0 / 32], cw[gi][b0 / 32 + 1], b0 % 32);
-            const uint32_t s1 = (b1 % 32 + BITS <= 32) ? (cw[gi][b1 / 32] >> (b1 % 32))
-                                                       : __funnelshift_r(cw[gi][b1 / 32], cw[gi][b1 / 32 + 1], b1 % 32);
-            const float v0 = __shfl_sync(kFull, ctab, (int)s0, L), v1 = __shfl_sync(kFull, ctab, (int)s1, L);
-            const __half2 hh = __floats2half2_rn(v0, v1);
-            hw[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+            const int b0 = (c8 * 8 + e) * BITS;
+            constexpr uint32_t MSK = (uint32_t)(A::PAIRS - 1) << 7;
+            uint32_t f;
+            if (b0 % 32 + 2 * BITS <= 32) {
+              const int sh = b0 % 32 - 7;
+              f = sh >= 0 ? (cw[gi][b0 / 32] >> sh) : (cw[gi][b0 / 32] << -sh);
+            } else {
+              f = __funnelshift_r(cw[gi][b0 / 32], cw[gi][b0 / 32 + 1], b0 % 32) << 7;
+            }
+            hw[e / 2] = lds32_addr(((f & MSK) | pt_lane) + pt_base);
           }
           *reinterpret_cast<uint4*>(a1 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
               make_uint4(hw[0], hw[1], hw[2], hw[3]);
         }
-        if (st2) {  // stage 2: +-1 from the sketch bits
+        if (st2) {  // stage 2: +-1 from the sketch bits, four per lookup
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
-            const uint32_t byte = sw[gi] >> (c8 * 8);
             uint32_t hw[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__shfl_sync(kFull, (int)ptab, (int)(byte >> (2 * e)), 4);
+            for (int e = 0; e < 2; ++e) {
+              const int b0 = c8 * 8 + 4 * e;
+              const uint32_t f = b0 >= 8 ? (sw[gi] >> (b0 - 8)) : (sw[gi] << (8 - b0));
+              const uint2 t2 = lds64_addr(((f & (15u << 8)) | st_lane) + st_base);
+              hw[2 * e] = t2.x;
+              hw[2 * e + 1] = t2.y;
+            }
             *reinterpret_cast<uint4*>(a2 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
                 make_uint4(hw[0], hw[1], hw[2], hw[3]);
           }
