@@ -39,7 +39,8 @@
  *    unspecified (but memory-safe) outputs.
  *
  * Layouts (row-major, rows contiguous, no padding between rows):
- *  - x, y   : [n, d] of dtype (IQ_DTYPE_F32 = float, IQ_DTYPE_F16 = IEEE half)
+ *  - x, y   : [n, d] of dtype (IQ_DTYPE_F32 = float, IQ_DTYPE_F16 = IEEE half,
+ *             IQ_DTYPE_BF16 = bfloat16); kernels compute in fp32 for every dtype
  *  - codes  : [n, iq_code_bytes_per_vector(d, bits)] uint8; row r holds the
  *             bitstream in which bit (j*bits + m) is bit m of coordinate j's
  *             code, byte B holding stream bits 8B..8B+7 from its LSB up.
@@ -82,7 +83,8 @@ typedef enum iq_variant {
 
 typedef enum iq_dtype {
   IQ_DTYPE_F32 = 0,
-  IQ_DTYPE_F16 = 1
+  IQ_DTYPE_F16 = 1,
+  IQ_DTYPE_BF16 = 2   /* bfloat16 storage (R28; not in the paper) */
 } iq_dtype;
 
 typedef struct iq_params iq_params; /* opaque, immutable after creation */

@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 __all__ = [
-    "FULL", "FAST", "PLANAR2D", "F32", "F16", "IQError", "Params", "HostPipeline", "lib",
+    "FULL", "FAST", "PLANAR2D", "F32", "F16", "BF16", "IQError", "Params", "HostPipeline", "lib",
     "iq_make_params", "iq_quantize", "iq_dequantize", "iq_roundtrip", "iq_error_sums",
     "iq_export_params", "iq_export_block_matrices", "iq_code_bytes_per_vector",
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
@@ -27,7 +27,7 @@ __all__ = [
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
-F32, F16 = 0, 1
+F32, F16, BF16 = 0, 1, 2
 VARIANTS = {"full": FULL, "fast": FAST, "planar2d": PLANAR2D, "2d": PLANAR2D}
 
 LIB_PATH = os.environ.get("IQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
@@ -185,7 +185,9 @@ def _dtype_code(t) -> int:
         return F32
     if t.dtype == torch.float16:
         return F16
-    raise TypeError(f"unsupported dtype {t.dtype} (float32 or float16)")
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(f"unsupported dtype {t.dtype} (float32, float16 or bfloat16)")
 
 
 def _stream_ptr(stream):

@@ -19,6 +19,9 @@ int launch_fast_f32(Kernel, int, int, const LaunchArgs&);
 int launch_fast_f16(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_f32(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_f16(Kernel, int, int, const LaunchArgs&);
+int launch_full_bf16(Kernel, int, int, const LaunchArgs&);
+int launch_fast_bf16(Kernel, int, int, const LaunchArgs&);
+int launch_planar2d_bf16(Kernel, int, int, const LaunchArgs&);
 
 bool attn_supported(int d) { return d == 64 || d == 128; }
 
@@ -29,10 +32,10 @@ bool gpu_supported(int d, int bits, int variant) {
 
 int launch(Kernel k, int variant, int dtype, int d, int bits, const LaunchArgs& a) {
   using Fn = int (*)(Kernel, int, int, const LaunchArgs&);
-  static const Fn table[3][2] = {{launch_full_f32, launch_full_f16},
-                                 {launch_fast_f32, launch_fast_f16},
-                                 {launch_planar2d_f32, launch_planar2d_f16}};
-  if (variant < 0 || variant > 2 || dtype < 0 || dtype > 1) return -1;
+  static const Fn table[3][3] = {{launch_full_f32, launch_full_f16, launch_full_bf16},
+                                 {launch_fast_f32, launch_fast_f16, launch_fast_bf16},
+                                 {launch_planar2d_f32, launch_planar2d_f16, launch_planar2d_bf16}};
+  if (variant < 0 || variant > 2 || dtype < 0 || dtype > 2) return -1;
   return table[variant][dtype](k, d, bits, a);
 }
 }  // namespace iq
@@ -61,13 +64,13 @@ iq_status cuda_fail(cudaError_t e, const char* what) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-size_t dtype_size(int dt) { return dt == IQ_DTYPE_F16 ? 2 : 4; }
+size_t dtype_size(int dt) { return dt == IQ_DTYPE_F32 ? 4 : 2; }
 
 // Common validation of a compute call.  Returns IQ_OK or the error.
 iq_status check_call(const iq_params* p, int dtype, int64_t n) {
   if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
-  if (dtype != IQ_DTYPE_F32 && dtype != IQ_DTYPE_F16)
-    return fail(IQ_ERR_INVALID_ARGUMENT, "dtype must be 0 (f32) or 1 (f16)");
+  if (dtype != IQ_DTYPE_F32 && dtype != IQ_DTYPE_F16 && dtype != IQ_DTYPE_BF16)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
   if (n < 0) return fail(IQ_ERR_INVALID_ARGUMENT, "n must be >= 0");
   if (p->device < 0 || !p->d_mat)
     return fail(IQ_ERR_DEVICE_MISMATCH, "params handle is host-only (device = -1)");
@@ -372,7 +375,7 @@ iq_status iq_error_sums(const iq_params* p, int dtype, int64_t n, const void* x,
   if (!x || !y || !sums) return fail(IQ_ERR_INVALID_ARGUMENT, "x, y and sums are required");
   if (!aligned(x, 16) || !aligned(y, 16) || !aligned(sums, 8))
     return fail(IQ_ERR_MISALIGNED, "x, y must be 16-byte and sums 8-byte aligned");
-  const int epc = dtype == IQ_DTYPE_F16 ? 8 : 4;
+  const int epc = dtype == IQ_DTYPE_F32 ? 4 : 8;
   const int64_t nchunks = n * p->hp.d / epc;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
@@ -382,6 +385,9 @@ iq_status iq_error_sums(const iq_params* p, int dtype, int64_t n, const void* x,
   if (dtype == IQ_DTYPE_F16)
     iq::k_error_sums<__half><<<(int)grid, iq::kThreads, 0, st>>>(
         nchunks, static_cast<const __half*>(x), static_cast<const __half*>(y), sums);
+  else if (dtype == IQ_DTYPE_BF16)
+    iq::k_error_sums<__nv_bfloat16><<<(int)grid, iq::kThreads, 0, st>>>(
+        nchunks, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(y), sums);
   else
     iq::k_error_sums<float><<<(int)grid, iq::kThreads, 0, st>>>(
         nchunks, static_cast<const float*>(x), static_cast<const float*>(y), sums);

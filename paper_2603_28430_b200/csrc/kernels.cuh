@@ -24,6 +24,7 @@
 // the whole kernel ("the entire block can often remain in
 // registers from input load through output store").
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -57,6 +58,26 @@ constexpr int kThreads = 256;                  // statistics kernel CTAs
 template <class T> struct DT;
 template <> struct DT<float> { static constexpr int EPC = 4; };
 template <> struct DT<__half> { static constexpr int EPC = 8; };
+template <> struct DT<__nv_bfloat16> { static constexpr int EPC = 8; };
+
+// two floats -> the packed 16-bit pair of T (round to nearest even [R15][R28])
+template <class T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// the packed 16-bit pair of T -> two floats (exact)
+template <class T> __device__ __forceinline__ float2 unpack2(uint32_t w);
+template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+template <> __device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
 
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 constexpr int clcm(int a, int b) { return a / cgcd(a, b) * b; }
@@ -329,15 +350,22 @@ template <> __device__ __forceinline__ void to_pairs<float>(const uint4& a, cons
   p[2] = f2(__uint_as_float(a.z), __uint_as_float(b.z));
   p[3] = f2(__uint_as_float(a.w), __uint_as_float(b.w));
 }
-template <> __device__ __forceinline__ void to_pairs<__half>(const uint4& a, const uint4& b, float2* p) {
+template <class T>
+__device__ __forceinline__ void to_pairs16(const uint4& a, const uint4& b, float2* p) {
   const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float2 ta = __half22float2(*reinterpret_cast<const __half2*>(&wa[k]));
-    const float2 tb = __half22float2(*reinterpret_cast<const __half2*>(&wb[k]));
+    const float2 ta = unpack2<T>(wa[k]);
+    const float2 tb = unpack2<T>(wb[k]);
     p[2 * k] = f2(ta.x, tb.x);
     p[2 * k + 1] = f2(ta.y, tb.y);
   }
+}
+template <> __device__ __forceinline__ void to_pairs<__half>(const uint4& a, const uint4& b, float2* p) {
+  to_pairs16<__half>(a, b, p);
+}
+template <> __device__ __forceinline__ void to_pairs<__nv_bfloat16>(const uint4& a, const uint4& b, float2* p) {
+  to_pairs16<__nv_bfloat16>(a, b, p);
 }
 // EPC coordinate pairs -> the two rows' 16-byte chunks (fp16: RN-even [R15])
 template <class T> __device__ __forceinline__ void from_pairs(const float2* p, uint4& a, uint4& b);
@@ -347,17 +375,22 @@ template <> __device__ __forceinline__ void from_pairs<float>(const float2* p, u
   b = make_uint4(__float_as_uint(p[0].y), __float_as_uint(p[1].y), __float_as_uint(p[2].y),
                  __float_as_uint(p[3].y));
 }
-template <> __device__ __forceinline__ void from_pairs<__half>(const float2* p, uint4& a, uint4& b) {
+template <class T>
+__device__ __forceinline__ void from_pairs16(const float2* p, uint4& a, uint4& b) {
   uint32_t wa[4], wb[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    __half2 ha = __floats2half2_rn(p[2 * k].x, p[2 * k + 1].x);
-    __half2 hb = __floats2half2_rn(p[2 * k].y, p[2 * k + 1].y);
-    wa[k] = *reinterpret_cast<uint32_t*>(&ha);
-    wb[k] = *reinterpret_cast<uint32_t*>(&hb);
+    wa[k] = pack2<T>(p[2 * k].x, p[2 * k + 1].x);
+    wb[k] = pack2<T>(p[2 * k].y, p[2 * k + 1].y);
   }
   a = make_uint4(wa[0], wa[1], wa[2], wa[3]);
   b = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+}
+template <> __device__ __forceinline__ void from_pairs<__half>(const float2* p, uint4& a, uint4& b) {
+  from_pairs16<__half>(p, a, b);
+}
+template <> __device__ __forceinline__ void from_pairs<__nv_bfloat16>(const float2* p, uint4& a, uint4& b) {
+  from_pairs16<__nv_bfloat16>(p, a, b);
 }
 
 // ----------------------------------------------------------- block operator
@@ -1042,10 +1075,7 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
           if constexpr (EPC == 8) {
             uint32_t w[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              __half2 h = __floats2half2_rn(out[i * 4 + k].x, out[i * 4 + k].y);
-              w[k] = *reinterpret_cast<uint32_t*>(&h);
-            }
+            for (int k = 0; k < 4; ++k) w[k] = pack2<T>(out[i * 4 + k].x, out[i * 4 + k].y);
             o = make_uint4(w[0], w[1], w[2], w[3]);
           } else {
             o = make_uint4(__float_as_uint(out[i * 2].x), __float_as_uint(out[i * 2].y),
@@ -1064,13 +1094,17 @@ template <> __device__ __forceinline__ void to_f32<float>(const uint4& r, float*
   f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
   f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
 }
-template <> __device__ __forceinline__ void to_f32<__half>(const uint4& r, float* f) {
+template <class T> __device__ __forceinline__ void to_f32_16(const uint4& r, float* f) {
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    const float2 t = unpack2<T>(w[k]);
     f[2 * k] = t.x; f[2 * k + 1] = t.y;
   }
+}
+template <> __device__ __forceinline__ void to_f32<__half>(const uint4& r, float* f) { to_f32_16<__half>(r, f); }
+template <> __device__ __forceinline__ void to_f32<__nv_bfloat16>(const uint4& r, float* f) {
+  to_f32_16<__nv_bfloat16>(r, f);
 }
 
 template <class T>
