@@ -49,9 +49,10 @@ struct AGeo {
   static constexpr int A_OFF = 0;                // [2 buffers][stage 1, stage 2]
   static constexpr int B_OFF = A_OFF + 4 * A_BYTES;
   static constexpr int QT_OFF = B_OFF + 2 * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
-  static constexpr int SIDE_OFF = QT_OFF + B_BYTES;    // per buffer: rho[128], gamma[128], scales[2][16]
+  static constexpr int NACC = 4;                 // accumulator / side-table buffers (TMEM is cheap)
+  static constexpr int SIDE_OFF = QT_OFF + B_BYTES;    // per accumulator: rho[128], gamma[128], scales[2][16]
   static constexpr int SIDE_BYTES = (2 * TILE + 2 * NQ) * 4;
-  static constexpr int QS_OFF = SIDE_OFF + 2 * SIDE_BYTES;   // the current head's scales [2][16]
+  static constexpr int QS_OFF = SIDE_OFF + NACC * SIDE_BYTES;   // the current head's scales [2][16]
   // lookup tables replicated across the 32 banks (entry e of lane l at
   // e * stride + 4 l, so every lane reads its own bank): a code PAIR -> half2
   // (C[c0], C[c1]), and 4 sketch bits -> 4 halves of +-1 (two words)
@@ -68,8 +69,8 @@ struct AGeo {
   static constexpr int W_PROD = NWD + NWE, W_MMA = NWD + NWE + 1;
   static constexpr int CTA_THREADS = 32 * (NWD + NWE + 2);
   static constexpr int GROUPS = D / 32;          // 32-coordinate groups per key
-  static constexpr int TMEM_COLS = 128;          // [2 buffers][stage 1, stage 2] x NQ, + NQ for S q
-  static constexpr int SQ_COL = 4 * NQ;
+  static constexpr int TMEM_COLS = 256;          // [NACC][stage 1, stage 2] x NQ, + NQ for S q
+  static constexpr int SQ_COL = 2 * NACC * NQ;
   static_assert(D == 64 || D == 128, "attention consumer: d in {64, 128}");
   static_assert(NST >= 3, "ring too shallow");
   static_assert(S_BYTES <= 4 * A_BYTES, "S staging");
@@ -106,9 +107,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   uint64_t* empty = full + NST;
   uint64_t* a_full = empty + NST;      // [2] decoders -> MMA
   uint64_t* a_free = a_full + 2;       // [2] MMA -> decoders (A buffer consumed)
-  uint64_t* acc_full = a_free + 2;     // [2] MMA -> epilogue
-  uint64_t* acc_empty = acc_full + 2;  // [2] epilogue -> MMA, decoders (accumulator and side table free)
-  uint64_t* s_bar = acc_empty + 2;     // S image staged (per head change)
+  uint64_t* acc_full = a_free + 2;     // [NACC] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + A::NACC;   // [NACC] epilogue -> MMA, decoders (accumulator, side table free)
+  uint64_t* s_bar = acc_empty + A::NACC;      // S image staged (per head change)
   uint64_t* sq_bar = s_bar + 1;        // S q MMA done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_bar + 1);
   uint8_t* ring = smem + A::RING_OFF;
@@ -116,10 +117,8 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWD); }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1);
-      mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], A::NWE);
-    }
+    for (int b = 0; b < 2; ++b) { mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1); }
+    for (int c = 0; c < A::NACC; ++c) { mbar_init(&acc_full[c], 1); mbar_init(&acc_empty[c], A::NWE); }
     mbar_init(s_bar, 1);
     mbar_init(sq_bar, 1);
     fence_mbar_init();
@@ -175,21 +174,21 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const uint32_t ab = smem_u32(a_base), bb = smem_u32(b_base);
       uint32_t j = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++j) {
-        const uint32_t b = j & 1;
+        const uint32_t b = j & 1, c = j % A::NACC, u = j / A::NACC;
         mbar_wait_tc(&a_full[b], (j >> 1) & 1);
-        mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);
+        mbar_wait_tc(&acc_empty[c], (u & 1) ^ 1);
         tc_fence_after();
 #pragma unroll 1
         for (int part = 0; part < (st2 ? 2 : 1); ++part) {
           const uint32_t ta = ab + (2 * b + part) * A::A_BYTES, tb = bb + part * A::B_BYTES;
-          const uint32_t td = tmem + (2 * b + part) * NQ;
+          const uint32_t td = tmem + (2 * c + part) * NQ;
 #pragma unroll
           for (int s = 0; s < D / 16; ++s)
             umma_f16(td, umma_desc_sw128(ta + umma_kstep_off(s, TILE)), umma_desc_sw128(tb + umma_kstep_off(s, NQ)),
                      idesc, s != 0);
         }
         umma_commit(&a_free[b]);
-        umma_commit(&acc_full[b]);
+        umma_commit(&acc_full[c]);
       }
     }
   } else if (warp >= NWD) {  // --------------------------------------------- epilogue
@@ -200,16 +199,16 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     int64_t h = t_begin / tph, k0 = (t_begin - h * tph) * TILE;
     for (int64_t t = t_begin; t < t_end; ++t, ++j, k0 += TILE) {
       if (k0 >= n_keys) { k0 = 0; ++h; }
-      const uint32_t b = j & 1;
-      mbar_wait_tc(&acc_full[b], (j >> 1) & 1);
+      const uint32_t c = j % A::NACC, u = j / A::NACC;
+      mbar_wait(&acc_full[c], u & 1);            // suspend-hint wait: the epilogue is off the critical path
       tc_fence_after();
       uint32_t v1[16], v2[16];
       const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16);
-      tmem_ld16(ta + (2 * b) * NQ, v1);
-      if (st2) tmem_ld16(ta + (2 * b + 1) * NQ, v2);
+      tmem_ld16(ta + (2 * c) * NQ, v1);
+      if (st2) tmem_ld16(ta + (2 * c + 1) * NQ, v2);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
-      const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + b * A::SIDE_BYTES);
+      const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + c * A::SIDE_BYTES);
       const int64_t k = k0 + row;
       if (k < n_keys) {
         const float rho = side[row], gam = side[TILE + row];
@@ -224,7 +223,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);   // accumulator and side table b are free
+      if (lane == 0) mbar_arrive(&acc_empty[c]);   // accumulator and side table c are free
     }
   } else {  // ------------------------------------------------------------- decoders
     // build the replicated lookup tables (once per CTA)
@@ -335,6 +334,20 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       asm volatile("bar.sync 1, %0;" ::"r"(NWD * 32) : "memory");   // B tiles, qs and the A buffers ready
     };
 
+    __builtin_assume(threadIdx.x < NWD * 32);
+    // per-thread constants of the decode mapping (thread g -> key g / GROUPS,
+    // 32-coordinate group g % GROUPS): stage word offsets, A-tile chunk offsets
+    constexpr int NG = TILE * GROUPS / (NWD * 32) > 0 ? TILE * GROUPS / (NWD * 32) : 1;
+    uint32_t coff[NG], qoff[NG], aoff[NG][4];
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) {
+      const int g = threadIdx.x + gi * NWD * 32;
+      const int gr = g / GROUPS, gs = g % GROUPS;
+      coff[gi] = (uint32_t)(gr * RB + gs * BITS * 4);
+      qoff[gi] = (uint32_t)(gr * QB + gs * 4);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) aoff[gi][c8] = umma_sw128_off(gr, gs * 32 + c8 * 8, TILE);
+    }
     int s = 0;
     uint32_t ph = 0, j = 0;
     int64_t hcur = -1;
@@ -363,7 +376,6 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       // decode mapping: thread g -> (key gr = g / GROUPS, group gs = g % GROUPS)
       // of 32 coordinates: BITS code words and one sketch word, contiguous in
       // the stage (consecutive lanes read consecutive words: no bank conflicts)
-      constexpr int NG = TILE * GROUPS / (NWD * 32) > 0 ? TILE * GROUPS / (NWD * 32) : 1;
       uint32_t cw[NG][BITS], sw[NG];
       float dep = 0.0f;
 #pragma unroll
@@ -371,10 +383,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         const int g = threadIdx.x + gi * NWD * 32;
         const int gr = g / GROUPS, gs = g % GROUPS;
         const bool gv = g < TILE * GROUPS && gr < nk;
-        if (full_tile) {           // everything is in the stage
+        if (full_tile && g < TILE * GROUPS) {   // everything is in the stage
 #pragma unroll
-          for (int i = 0; i < BITS; ++i) cw[gi][i] = gv ? lds32(stg + A::C_OFF + gr * RB + (gs * BITS + i) * 4) : 0u;
-          sw[gi] = (st2 && gv) ? lds32(stg + A::Q_OFF + gr * QB + gs * 4) : 0u;
+          for (int i = 0; i < BITS; ++i) cw[gi][i] = lds32(stg + A::C_OFF + coff[gi] + 4 * i);
+          sw[gi] = st2 ? lds32(stg + A::Q_OFF + qoff[gi]) : 0u;
         } else {
 #pragma unroll
           for (int i = 0; i < BITS; ++i) {
@@ -406,8 +418,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       __syncwarp();
       if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
       mbar_wait_tc(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
-      mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);   // side table b read by the epilogue of tile j - 2
-      float* side = reinterpret_cast<float*>(smem + A::SIDE_OFF + b * A::SIDE_BYTES);
+      const uint32_t ca = j % A::NACC;
+      mbar_wait_tc(&acc_empty[ca], ((j / A::NACC) & 1) ^ 1);   // side table read by the epilogue of tile j - NACC
+      float* side = reinterpret_cast<float*>(smem + A::SIDE_OFF + ca * A::SIDE_BYTES);
       if (threadIdx.x < 2 * TILE) side[threadIdx.x] = rg;
       if (threadIdx.x < 2 * NQ) side[2 * TILE + threadIdx.x] = qs_mine;
       uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
@@ -436,8 +449,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
             }
             hw[e / 2] = lds32_addr(((f & MSK) | pt_lane) + pt_base);
           }
-          *reinterpret_cast<uint4*>(a1 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
-              make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(a1 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         }
         if (st2) {  // stage 2: +-1 from the sketch bits, four per lookup
 #pragma unroll
@@ -451,8 +463,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
               hw[2 * e] = t2.x;
               hw[2 * e + 1] = t2.y;
             }
-            *reinterpret_cast<uint4*>(a2 + umma_sw128_off(gr, gs * 32 + c8 * 8, TILE)) =
-                make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(a2 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
           }
         }
       }
