@@ -68,14 +68,29 @@ def parse_args():
     return ap.parse_args()
 
 
+def config_name(a):
+    """Which BASELINE.json configs[] entry the arguments describe."""
+    key = (a.variant, a.d, a.bits, a.dtype)
+    if key == ("fast", 128, 4, "f16") and a.n == 32 * 8 * 32768:
+        return "configs[2] KV-cache shaped (32 layers x 8 KV heads x 32k tokens)"
+    if a.d == 256 and a.bits == 2 and a.dtype == "f16" and a.n == 1 << 24:
+        return "configs[3] 16M vectors (2D vs Full/Fast on the same inputs)"
+    if key == ("full", 512, 2, "f16") and a.n == 1 << 26:
+        return "configs[4] 64M vectors (bandwidth saturation)"
+    if a.n == 1 << 20 and key == ("full", 128, 3, "f16"):
+        return "configs[1] headline"
+    return "configs[1] setting" if a.n == 1 << 20 else "custom"
+
+
 def workload_config(a, world):
     return {
-        "workload": (f"configs[1] headline: IsoQuant-{a.variant.capitalize()} d={a.d} b={a.bits} "
+        "workload": (f"{config_name(a)}: IsoQuant-{a.variant.capitalize()} d={a.d} b={a.bits} "
                      f"{'fp16' if a.dtype == 'f16' else 'fp32'}, {a.n} synthetic unit vectors per GPU"),
         "variant": a.variant, "d": a.d, "bits": a.bits, "io_dtype": a.dtype, "n_per_gpu": a.n,
         "global_vectors": a.n * world, "parallelism": f"dp{world} (vectors sharded by batch)",
         "step": "one fused roundtrip launch (iq_roundtrip) over the batch",
-        "l2": "inputs larger than L2 (>=256 MiB per buffer vs 126 MB) and 2 rotating buffer sets",
+        "l2": "inputs larger than L2 (>=256 MiB per buffer vs 126 MB) and 2 rotating buffer sets "
+              "(1 set, or in place, when they do not fit HBM)",
     }
 
 
@@ -274,9 +289,17 @@ def main():
     p = iq.iq_make_params(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=local)
     stream = torch.cuda.current_stream()
     # each rank's shard: its own chunk seeds (weak scaling, no data movement)
+    # two rotating buffer sets while they fit; one set (y separate) or in place
+    # (y = x, allowed by the ABI) for the largest configs (cfg5: 64 GiB per buffer)
+    buf = a.n * a.d * s
+    free_b = torch.cuda.mem_get_info(dev)[0]
+    nsets = 2 if 4 * buf <= 0.8 * free_b else 1
+    inplace = nsets == 1 and 2 * buf > 0.8 * free_b
     xs = [iqsynth.device_unit_vectors(a.n, a.d, D.shard_seed(2, rank, j), tdt, dev)
-          for j in range(2)]
-    ys = [torch.empty_like(x) for x in xs]
+          for j in range(nsets)]
+    ys = xs if inplace else [torch.empty_like(x) for x in xs]
+    if nsets == 1:
+        xs, ys = xs * 2, ys * 2
 
     def step(i):
         iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], stream=stream)
@@ -314,7 +337,7 @@ def main():
     for j in range(2):
         iq.iq_error_sums(p, xs[j], ys[j], sums)
     ms_max, se_tot, _, cnt_tot = D.combine_stats(ms, *sums.tolist(), 2.0 * a.n * a.d, device=dev)
-    mse = se_tot / cnt_tot
+    mse = None if inplace else se_tot / cnt_tot
 
     ms_step = ms_max / a.steps
     value = world * a.n / (ms_step / 1e3)
