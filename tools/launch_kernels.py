@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kernel", default="roundtrip",
-                    choices=["roundtrip", "roundtrip_emit", "quantize", "dequantize", "quantize_qjl", "all"])
+                    choices=["roundtrip", "roundtrip_emit", "quantize", "dequantize", "quantize_qjl", "attention", "all"])
     ap.add_argument("--variant", default="full")
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--bits", type=int, default=3)
@@ -31,11 +31,17 @@ def main():
     codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
     norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
     iq.iq_quantize(p, x, codes, norms)
-    if a.kernel == "quantize_qjl":
+    if a.kernel in ("quantize_qjl", "attention", "all"):
         pq = iq.iq_make_params_qjl(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
         qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device="cuda")
         rn = torch.empty(a.n, dtype=torch.float32, device="cuda")
-    kinds = ["quantize", "dequantize", "roundtrip", "roundtrip_emit"] if a.kernel == "all" else [a.kernel]
+    kinds = (["quantize", "dequantize", "roundtrip", "roundtrip_emit", "quantize_qjl", "attention"]
+             if a.kernel == "all" else [a.kernel])
+    if "attention" in kinds:       # the batch as a cache of 32 heads, 4 queries per head
+        H = 32
+        nk = a.n // H
+        qh = torch.randn((H, 4, a.d), dtype=tdt, device="cuda")
+        iq.iq_quantize_qjl(pq, x, codes, norms, qj, rn)
     for k in kinds:
         for _ in range(a.reps):
             if k == "roundtrip":
@@ -46,6 +52,9 @@ def main():
                 iq.iq_quantize(p, x, codes, norms)
             elif k == "quantize_qjl":
                 iq.iq_quantize_qjl(pq, x, codes, norms, qj, rn)
+            elif k == "attention":
+                iq.iq_attention_scores(pq, codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk), qh,
+                                       qj[:H * nk].view(H, nk, -1), rn[:H * nk].view(H, nk))
             else:
                 iq.iq_dequantize(p, codes, norms, y=y)
     torch.cuda.synchronize()
