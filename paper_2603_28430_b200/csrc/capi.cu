@@ -46,6 +46,7 @@ struct iq_params {
   float* d_mat = nullptr;
   uint8_t* d_qjl = nullptr;   // UMMA image of the stage-2 sketch S (iq_make_params_qjl)
   uint8_t* d_qjl_a = nullptr; // the same S as a 128-row A operand (attention consumer)
+  uint8_t* d_qjl_rot = nullptr; // S' = S M^T as fp16 hi + lo B images (16-bit sketch kernel)
 };
 
 namespace {
@@ -157,6 +158,9 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
     if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl, p->hp.qjl_img.size());
     if (e == cudaSuccess && qjl)
       e = cudaMemcpy(p->d_qjl, p->hp.qjl_img.data(), p->hp.qjl_img.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl_rot, p->hp.qjl_img_rot.size());
+    if (e == cudaSuccess && qjl)
+      e = cudaMemcpy(p->d_qjl_rot, p->hp.qjl_img_rot.data(), p->hp.qjl_img_rot.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl_a, p->hp.qjl_img_a.size());
     if (e == cudaSuccess && qjl)
       e = cudaMemcpy(p->d_qjl_a, p->hp.qjl_img_a.data(), p->hp.qjl_img_a.size(), cudaMemcpyHostToDevice);
@@ -165,6 +169,7 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
       if (p->d_mat) cudaFree(p->d_mat);
       if (p->d_qjl) cudaFree(p->d_qjl);
       if (p->d_qjl_a) cudaFree(p->d_qjl_a);
+      if (p->d_qjl_rot) cudaFree(p->d_qjl_rot);
       delete p;
       return cuda_fail(e, "iq_make_params device upload");
     }
@@ -190,6 +195,7 @@ iq_status iq_free_params(iq_params* p) {
     cudaFree(p->d_mat);
     if (p->d_qjl) cudaFree(p->d_qjl);
     if (p->d_qjl_a) cudaFree(p->d_qjl_a);
+    if (p->d_qjl_rot) cudaFree(p->d_qjl_rot);
     if (prev >= 0 && prev != p->device) cudaSetDevice(prev);
   }
   delete p;
@@ -278,6 +284,7 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
   a.codes = codes;
   a.norms = norms;
   a.qjl_img = p->d_qjl;
+  a.qjl_img_rot = p->d_qjl_rot;
   a.qjl = qjl;
   a.rnorms = rnorms;
   return run(iq::Kernel::kQuantizeQjl, p, dtype, a);

@@ -54,6 +54,10 @@ struct HostParams {
   std::vector<uint16_t> qjl_half;
   std::vector<uint8_t> qjl_img;
   std::vector<uint8_t> qjl_img_a;   // the same S as a 128-row A operand (rows >= m zero)
+  // S' = S M^T (M the fp32 block operators of mat): z = S r = S' (M r), so the
+  // 16-bit sketch kernel works on the forward-rotated residual; fp16 hi and
+  // lo parts (S' to ~2^-22), two K-major 128B-swizzled B images back to back
+  std::vector<uint8_t> qjl_img_rot;
 };
 
 // Sketch generator key and layout (params.cpp).
@@ -96,6 +100,7 @@ struct LaunchArgs {
   const uint8_t* qjl_in;
   const float* rnorms_in;
   const uint8_t* qjl_img_a;
+  const uint8_t* qjl_img_rot;
   double* sums;
   void* stream;
   const uint8_t* qjl_img;   // device UMMA image of S (stage 2)

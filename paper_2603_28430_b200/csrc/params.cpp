@@ -14,6 +14,8 @@
 //    fit unspecified, reading [R1]), exactly symmetrised [R2], scaled by
 //    1/sqrt(d), rounded to fp32; thresholds are fp32 midpoints of adjacent
 //    fp32 centroids [R14b].
+#include <cuda_fp16.h>
+
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -338,6 +340,31 @@ bool build_qjl(HostParams* hp, std::string* err) {
     for (int i = 0; i < m; ++i)
       for (int k = 0; k < d; ++k)
         std::memcpy(&hp->qjl_img_a[umma_sw128_off(i, k, 128)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
+  }
+  hp->qjl_img_rot.clear();
+  if (qjl_supported(d)) {
+    const int pw = hp->variant == IQ_VARIANT_PLANAR2D ? 2 : 4;
+    const size_t img = static_cast<size_t>(m) * d * 2;
+    hp->qjl_img_rot.assign(2 * img, 0);
+    for (int i = 0; i < m; ++i)
+      for (int b = 0; b < d / pw; ++b)
+        for (int j = 0; j < pw; ++j) {
+          // S'[i][pw b + j] = sum_c S[i][pw b + c] M_b[j][c]   (S' = S M^T)
+          double acc = 0.0;
+          for (int c = 0; c < pw; ++c) {
+            __half_raw hr;
+            hr.x = hp->qjl_half[static_cast<size_t>(i) * d + pw * b + c];
+            acc += static_cast<double>(__half2float(__half(hr))) *
+                   static_cast<double>(hp->mat[static_cast<size_t>(pw * pw) * b + pw * j + c]);
+          }
+          const uint16_t hi = half_rn(acc);
+          __half_raw hh;
+          hh.x = hi;
+          const uint16_t lo = half_rn(acc - static_cast<double>(__half2float(__half(hh))));
+          const uint32_t off = umma_sw128_off(i, pw * b + j, m);
+          std::memcpy(&hp->qjl_img_rot[off], &hi, 2);
+          std::memcpy(&hp->qjl_img_rot[img + off], &lo, 2);
+        }
   }
   hp->has_qjl = true;
   return true;

@@ -26,12 +26,16 @@ namespace iq {
 template <class T, int D, int BITS, int VAR>
 struct QGeo {
   using Gm = Geo<T, D, BITS, VAR, 2>;            // stage-1 lane geometry of the code-emitting kernels
+#ifndef IQ_QJL_ROTD
+#define IQ_QJL_ROTD 1
+#endif
 #ifdef IQ_QJL_NWC
   static constexpr int NWC0 = IQ_QJL_NWC;
 #else
-  // measured: 16 warps (96-register cap, small spills) win at b <= 2 fp16, 8
-  // warps (no spills) elsewhere
-  static constexpr int NWC0 = (sizeof(T) == 2 && BITS <= 2) ? 16 : 8;
+  // measured: 16 warps for 16-bit rows at b <= 3 (the rotated-domain
+  // residual fits the 96-register cap without spills), 8 at b = 4 and for
+  // fp32 (whose inverse-rotation path would spill)
+  static constexpr int NWC0 = (sizeof(T) == 2 && BITS <= 3) ? 16 : 8;
 #endif
   // compute warps: a multiple of 4 (TMEM lane quadrants), each with at least
   // one row pair per lane group of the 128-row tile
@@ -41,12 +45,16 @@ struct QGeo {
   static constexpr int M = D;                    // sketch rows (m = d, R20)
   static constexpr int ROWB = D * (int)sizeof(T);
   static constexpr int STAGE = TILE * ROWB;      // 32 KB (fp16) / 64 KB (fp32 at d = 128)
-  static constexpr int NST = sizeof(T) == 2 ? 3 : 2;
+  static constexpr int NST = 2;
+  // 16-bit rows: residual in the rotated domain, r' = T x - rho C[code]
+  // (no inverse rotation), against S' = S M^T as fp16 hi + lo (3 MMA passes)
+  static constexpr bool ROTD = sizeof(T) == 2 && IQ_QJL_ROTD;
   static constexpr int A_BYTES = TILE * D * 2;   // one fp16 operand tile (hi or lo)
   static constexpr int S_BYTES = M * D * 2;
+  static constexpr int B_BYTES = ROTD ? 2 * S_BYTES : S_BYTES;   // the B image(s) in shared memory
   static constexpr int A_OFF = NST * STAGE;      // 1024-aligned (STAGE is)
   static constexpr int S_OFF = A_OFF + 2 * A_BYTES;
-  static constexpr int BAR_OFF = S_OFF + S_BYTES;
+  static constexpr int BAR_OFF = S_OFF + B_BYTES;
   static constexpr int OPS_OFF = BAR_OFF + 256;   // stage-1 operators (when Gm::OPS_SMEM)
   static constexpr int SMEM = OPS_OFF + Gm::OPS_BYTES + 1024;   // + slack to align the base to 1024
   static constexpr int CW = M / (NWC / 4);        // sketch columns per epilogue warp
@@ -192,8 +200,8 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
   if (warp == NWC) {  // ------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      mbar_arrive_expect_tx(s_bar, Q::S_BYTES);
-      bulk_g2s(s_sm, s_img, Q::S_BYTES, s_bar, policy_evict_last());     // every CTA reads S
+      mbar_arrive_expect_tx(s_bar, Q::B_BYTES);
+      bulk_g2s(s_sm, s_img, Q::B_BYTES, s_bar, policy_evict_last());     // every CTA reads S (S' hi, lo)
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -219,12 +227,14 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         mbar_wait_tc(&acc_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t td = tmem + b * M;
+        // A_hi B_hi + A_lo B_hi (+ A_hi B_lo with S' split in two)
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {
+        for (int part = 0; part < (Q::ROTD ? 3 : 2); ++part) {
+          const uint32_t pa = part == 1 ? al : ah, pb = sb + (part == 2 ? Q::S_BYTES : 0);
 #pragma unroll
           for (int s = 0; s < D / 16; ++s)
-            umma_f16(td, umma_desc_sw128((part ? al : ah) + umma_kstep_off(s, TILE)),
-                     umma_desc_sw128(sb + umma_kstep_off(s, M)), idesc, (part | s) != 0);
+            umma_f16(td, umma_desc_sw128(pa + umma_kstep_off(s, TILE)), umma_desc_sw128(pb + umma_kstep_off(s, M)),
+                     idesc, (part | s) != 0);
         }
         umma_commit(a_free);
         umma_commit(&acc_full[b]);
@@ -247,6 +257,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
       load_ops<Gm>(mat, sub, P);
     }
     const float ctab = cb.cent[lane & ((1 << BITS) - 1)];
+    const float inv_gscale = 1.0f / cb.gscale;       // a power of two: exact
     const float gtab = cb.gtab[lane];
     const uint32_t gcode = cb.gcode[lane];
     const int quad = warp & 3, part = warp >> 2;      // TMEM lane quadrant, column slice
@@ -315,6 +326,9 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
           ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
         const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
         const float2 rinv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
+        const float2 nrho = f2(-rho.x, -rho.y);
+        // max(rho, eps) / S: undoes the grid's scaling of the rotated row (ROTD, b = 4)
+        const float2 isc = mul2(f2(fmaxf(rho.x, 1e-12f), fmaxf(rho.y, 1e-12f)), bc(inv_gscale));
 
         // ---- stage 1: codes (the iq_quantize rule) and x^ in fp32
         float2 out[EPL];
@@ -341,7 +355,12 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
               cq[jv] = f2(sign_xor(__shfl_sync(kFull, gtab, (int)ia), yb[jv].x),
                           sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[jv].y));
             }
-            rot_inv<PW>(Mb, cq, out + b * PW);          // T^-1(C[code]); rho applied with r below
+            if constexpr (Q::ROTD) {                   // r' = T x - rho c, T x = yb max(rho, eps) / S
+#pragma unroll
+              for (int jv = 0; jv < PW; ++jv) out[b * PW + jv] = fma2(cq[jv], nrho, mul2(yb[jv], isc));
+            } else {
+              rot_inv<PW>(Mb, cq, out + b * PW);        // T^-1(C[code]); rho applied with r below
+            }
           }
         } else {
           RowQ<BITS> q;
@@ -361,8 +380,13 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
             for (int e = 0; e < EPC; ++e)
               cq[e] = f2(__shfl_sync(kFull, ctab, (int)(cwa[i] >> (e * BITS)), 1 << BITS),
                          __shfl_sync(kFull, ctab, (int)(cwb[i] >> (e * BITS)), 1 << BITS));
+            if constexpr (Q::ROTD) {                     // r' = T x - rho c
 #pragma unroll
-            for (int bb = 0; bb < BPCH; ++bb) rot_inv<PW>(Mc[bb], cq + bb * PW, out + i * EPC + bb * PW);
+              for (int e = 0; e < EPC; ++e) out[i * EPC + e] = fma2(cq[e], nrho, yb[e]);
+            } else {
+#pragma unroll
+              for (int bb = 0; bb < BPCH; ++bb) rot_inv<PW>(Mc[bb], cq + bb * PW, out + i * EPC + bb * PW);
+            }
           }
         }
         // codes + norms (bit-identical to iq_quantize)
@@ -376,12 +400,12 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
             if (okb) *reinterpret_cast<uint32_t*>(ct + off + VPW * RB) = wb;
           }
         }
-        // ---- residual r = x - rho T^-1(C[code]) (R21), gamma = ||r|| (R23)
-        const float2 nrho = f2(-rho.x, -rho.y);
+        // ---- residual r = x - rho T^-1(C[code]) (R21) -- or r' = T r in the
+        // rotated domain (ROTD); gamma = ||r|| = ||r'|| (R23)
         float2 g2 = bc(0.0f);
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
-          out[e] = fma2(out[e], nrho, v[e]);
+          if constexpr (!Q::ROTD) out[e] = fma2(out[e], nrho, v[e]);
           g2 = fma2(out[e], out[e], g2);
         }
 #pragma unroll
