@@ -64,7 +64,10 @@ struct AGeo {
   static constexpr int RING_MAX = 227 * 1024 - RING_OFF - 1024;
   static constexpr int NST = (RING_MAX / STAGE) < 16 ? (RING_MAX / STAGE) : 16;
   static constexpr int SMEM = RING_OFF + NST * STAGE + 1024;
-  static constexpr int NWD = 16;                 // decoder warps
+#ifndef IQ_ATTN_NWD
+#define IQ_ATTN_NWD 16
+#endif
+  static constexpr int NWD = IQ_ATTN_NWD;        // decoder warps
   static constexpr int NWE = 4;                  // epilogue warps (one per TMEM lane quadrant)
   static constexpr int W_PROD = NWD + NWE, W_MMA = NWD + NWE + 1;
   static constexpr int CTA_THREADS = 32 * (NWD + NWE + 2);
@@ -337,7 +340,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     __builtin_assume(threadIdx.x < NWD * 32);
     // per-thread constants of the decode mapping (thread g -> key g / GROUPS,
     // 32-coordinate group g % GROUPS): stage word offsets, A-tile chunk offsets
-    constexpr int NG = TILE * GROUPS / (NWD * 32) > 0 ? TILE * GROUPS / (NWD * 32) : 1;
+    constexpr int NG = (TILE * GROUPS + NWD * 32 - 1) / (NWD * 32);   // groups per thread
     uint32_t coff[NG], qoff[NG], aoff[NG][4];
 #pragma unroll
     for (int gi = 0; gi < NG; ++gi) {

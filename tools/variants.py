@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "tchint": ["-DIQ_TC_SPIN=0"],
+    "attn8": ["-DIQ_ATTN_NWD=8"],
+    "attn12": ["-DIQ_ATTN_NWD=12"],
 }
 
 
