@@ -112,7 +112,8 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   uint64_t* a_free = a_full + 2;       // [2] MMA -> decoders (A buffer consumed)
   uint64_t* acc_full = a_free + 2;     // [NACC] MMA -> epilogue
   uint64_t* acc_empty = acc_full + A::NACC;   // [NACC] epilogue -> MMA, decoders (accumulator, side table free)
-  uint64_t* s_bar = acc_empty + A::NACC;      // S image staged (per head change)
+  uint64_t* side_full = acc_empty + A::NACC;  // [NACC] decoders -> epilogue: side table written
+  uint64_t* s_bar = side_full + A::NACC;      // S image staged (per head change)
   uint64_t* sq_bar = s_bar + 1;        // S q MMA done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_bar + 1);
   uint8_t* ring = smem + A::RING_OFF;
@@ -121,7 +122,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWD); }
     for (int b = 0; b < 2; ++b) { mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1); }
-    for (int c = 0; c < A::NACC; ++c) { mbar_init(&acc_full[c], 1); mbar_init(&acc_empty[c], A::NWE); }
+    for (int c = 0; c < A::NACC; ++c) {
+      mbar_init(&acc_full[c], 1); mbar_init(&acc_empty[c], A::NWE);
+      mbar_init(&side_full[c], (2 * TILE) / 32);   // the warps that write rho / gamma / scales
+    }
     mbar_init(s_bar, 1);
     mbar_init(sq_bar, 1);
     fence_mbar_init();
@@ -211,6 +215,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       if (st2) tmem_ld16(ta + (2 * c + 1) * NQ, v2);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
+      mbar_wait(&side_full[c], u & 1);            // ordinary release/acquire for the side table
       const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + c * A::SIDE_BYTES);
       const int64_t k = k0 + row;
       if (k < n_keys) {
@@ -426,6 +431,10 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       float* side = reinterpret_cast<float*>(smem + A::SIDE_OFF + ca * A::SIDE_BYTES);
       if (threadIdx.x < 2 * TILE) side[threadIdx.x] = rg;
       if (threadIdx.x < 2 * NQ) side[2 * TILE + threadIdx.x] = qs_mine;
+      if (threadIdx.x < 2 * TILE) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&side_full[ca]);
+      }
       uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
       uint8_t* a2 = a1 + A::A_BYTES;
 #pragma unroll
