@@ -4,7 +4,7 @@
   python tools/variants.py time [--d 128 --bits 3 --dtype f16 --variant full]
                                             # on the GPU box: time each variant
 
-Variants differ only in compile-time knobs (-DIQ_RING_KB, -DIQ_PAIR_UNROLL); the product build is the default one.
+Variants differ only in compile-time knobs (see VARIANTS); the product build is the default one.
 """
 import argparse
 import json
@@ -17,8 +17,13 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "attn8": ["-DIQ_ATTN_NWD=8"],
-    "attn12": ["-DIQ_ATTN_NWD=12"],
+    "opsreg": ["-DIQ_OPS_SMEM=0"],          # encoder operators always in registers (8-warp CTAs)
+    "nwc12": ["-DIQ_NWC_WIDE=12"],          # 12 compute warps in the wide encoder CTAs
+    "b3fma": ["-DIQ_B3_ALU=0"],             # b = 3 chain as FSET + FFMA2
+    "stage64": ["-DIQ_STAGE_KB=64"],        # 64 KB ring stages
+    "tchint": ["-DIQ_TC_SPIN=0"],           # suspend-hint waits on tcgen05.commit barriers
+    "qjl8": ["-DIQ_QJL_NWC=8"],             # 8 compute warps in the stage-2 kernel
+    "attn8": ["-DIQ_ATTN_NWD=8"],           # 8 decoder warps in the attention consumer
 }
 
 
