@@ -245,6 +245,37 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
                               const float* rnorms, int n_q, const void* q, float* scores,
                               void* cuda_stream);
 
+/* ------------------------------------------------------------------------
+ * Learning the rotations (PAPER.md "Parameterization and Learning",
+ * q = u / ||u|| with free u; R29, R30).  Objective:
+ * the stage-1 distortion on normalised rows L = sum_rows ||T xbar - Q(T xbar)||^2,
+ * whose gradient is exact almost everywhere (Q is piecewise constant).  A
+ * training step: iq_distortion_grad (GPU, dL/dM per block) ->
+ * iq_rot_grad_from_operator_grad (host, chain rule to the parameters) ->
+ * rot <- rot - lr * grad_rot -> iq_make_params_explicit (renormalises).
+ * ------------------------------------------------------------------------ */
+
+/* Parameters from explicit rotations in the iq_export_params layout (Full
+ * [g][8] = q_L, q_R; Fast [g][4]; 2D [g2][2] = (cos, sin)); each quaternion /
+ * pair is normalised on input.  No stage-2 sketch. */
+iq_status iq_make_params_explicit(int d, int bits, int variant, const double* rot, size_t rot_len,
+                                  int device, iq_params** out);
+
+/* GPU: grad[b][i][j] += dL/dM_b[i][j] = 2 sum_rows e_i xbar_j with e = T xbar
+ * - Q(T xbar), per block operator (DEVICE buffer of block_matrix_count doubles:
+ * 16 per 4-D block, 4 per 2-D pair; caller zeroes it); loss (nullable DEVICE
+ * double) += L.  One kernel; fp32 per-row math, fp64 accumulation across
+ * CTAs. */
+iq_status iq_distortion_grad(const iq_params* p, int dtype, int64_t n, const void* x, double* grad,
+                             double* loss, void* cuda_stream);
+
+/* Host: chain rule from dL/dM (host copy of the iq_distortion_grad output)
+ * to the rotation parameters (iq_export_params layout), each unit vector's
+ * gradient projected on its tangent space (the gradient w.r.t. u at
+ * ||u|| = 1). */
+iq_status iq_rot_grad_from_operator_grad(const iq_params* p, const double* G, size_t G_len,
+                                         double* grad_rot, size_t rot_len);
+
 /*
  * iq_error_sums — reconstruction statistics on the device (not part of the
  * timed path): sums[0] += sum_{i,j} (x_ij - y_ij)^2, sums[1] += sum x_ij^2,

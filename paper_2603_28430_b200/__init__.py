@@ -23,7 +23,7 @@ __all__ = [
     "iq_export_params", "iq_export_block_matrices", "iq_code_bytes_per_vector",
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
     "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
-    "iq_attention_scores",
+    "iq_attention_scores", "iq_make_params_explicit", "iq_distortion_grad", "iq_rot_grad_from_operator_grad",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -64,6 +64,9 @@ _sig = {
     "iq_quantize_qjl": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
     "iq_attention_scores": (_c_int, [_c_vp, _c_int, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_vp,
                                      _c_vp, _c_vp]),
+    "iq_make_params_explicit": (_c_int, [_c_int, _c_int, _c_int, _c_vp, _c_sz, _c_int, ctypes.POINTER(_c_vp)]),
+    "iq_distortion_grad": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "iq_rot_grad_from_operator_grad": (_c_int, [_c_vp, _c_vp, _c_sz, _c_vp, _c_sz]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -153,6 +156,26 @@ def iq_export_qjl_matrix(p: Params) -> np.ndarray:
     S = np.zeros((p.d, p.d), dtype=np.float32)
     _check(lib.iq_export_qjl_matrix(p.handle, S.ctypes.data, S.size), "iq_export_qjl_matrix")
     return S
+
+
+def iq_make_params_explicit(d: int, bits: int, variant, rot, device: int = 0) -> Params:
+    """Parameters from explicit rotations (iq_export_params layout, fp64)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant.lower()]
+    r = np.ascontiguousarray(rot, dtype=np.float64)
+    h = ctypes.c_void_p()
+    _check(lib.iq_make_params_explicit(int(d), int(bits), int(variant), r.ctypes.data, r.size, int(device),
+                                       ctypes.byref(h)), "iq_make_params_explicit")
+    return Params(h.value, d, bits, variant, 0, device)
+
+
+def iq_rot_grad_from_operator_grad(p: Params, G) -> np.ndarray:
+    """Host chain rule: dL/dM (array of block_matrix_count doubles) -> dL/d(rot)."""
+    g = np.ascontiguousarray(G, dtype=np.float64)
+    out = np.zeros(iq_rotation_param_count(p.d, p.variant), dtype=np.float64)
+    _check(lib.iq_rot_grad_from_operator_grad(p.handle, g.ctypes.data, g.size, out.ctypes.data, out.size),
+           "iq_rot_grad_from_operator_grad")
+    return out
 
 
 def iq_export_params(p: Params) -> dict:
@@ -289,6 +312,21 @@ def iq_attention_scores(p: Params, codes, norms, q, qjl=None, rnorms=None, score
                                    _ptr(rnorms), n_q, _ptr(q), _ptr(scores), _stream_ptr(stream)),
            "iq_attention_scores")
     return scores
+
+
+def iq_distortion_grad(p: Params, x, grad=None, loss=None, stream=None):
+    """dL/dM per block operator (device fp64, accumulated) and the distortion
+    L (device fp64 scalar, accumulated) over the rows of x."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    nm = (4 * ((p.d + 1) // 2)) if p.variant == PLANAR2D else (16 * ((p.d + 3) // 4))
+    if grad is None:
+        grad = torch.zeros(nm, dtype=torch.float64, device=x.device)
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float64, device=x.device)
+    _check(lib.iq_distortion_grad(p.handle, _dtype_code(x), n, _ptr(x), _ptr(grad), _ptr(loss),
+                                  _stream_ptr(stream)), "iq_distortion_grad")
+    return grad, loss
 
 
 def iq_error_sums(p: Params, x, y, sums=None, stream=None):

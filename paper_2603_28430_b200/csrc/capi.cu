@@ -126,14 +126,14 @@ const char* iq_status_string(iq_status s) {
 const char* iq_last_error_detail(void) { return g_detail.c_str(); }
 
 static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, int device, bool qjl,
-                                  iq_params** out) {
+                                  iq_params** out, const double* rot_in = nullptr) {
   if (!out) return fail(IQ_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (device < -1) return fail(IQ_ERR_INVALID_ARGUMENT, "device must be >= -1");
   iq_params* p = new (std::nothrow) iq_params();
   if (!p) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
   std::string err;
-  if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err) ||
+  if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err, rot_in) ||
       (qjl && !iq::build_qjl(&p->hp, &err))) {
     delete p;
     return fail(IQ_ERR_INVALID_ARGUMENT, err);
@@ -184,6 +184,23 @@ iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device
 
 iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int device, iq_params** out) {
   return make_params_impl(d, bits, variant, seed, device, true, out);
+}
+
+iq_status iq_make_params_explicit(int d, int bits, int variant, const double* rot, size_t rot_len, int device,
+                                  iq_params** out) {
+  if (!rot) return fail(IQ_ERR_INVALID_ARGUMENT, "rot is NULL");
+  if (d < 1 || rot_len < iq::rotation_param_count(d, variant))
+    return fail(IQ_ERR_BUFFER_TOO_SMALL, "rot shorter than iq_rotation_param_count(d, variant)");
+  return make_params_impl(d, bits, variant, 0, device, false, out, rot);
+}
+
+iq_status iq_rot_grad_from_operator_grad(const iq_params* p, const double* G, size_t G_len, double* grad_rot,
+                                         size_t rot_len) {
+  if (!p || !G || !grad_rot) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (G_len < p->hp.mat.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "G shorter than the block operators");
+  if (rot_len < p->hp.rot.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "grad_rot shorter than the rotation params");
+  iq::operator_grad_to_rot(p->hp, G, grad_rot);
+  return IQ_OK;
 }
 
 iq_status iq_free_params(iq_params* p) {
@@ -322,6 +339,21 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
   a.rnorms_in = rnorms;
   a.qjl_img_a = p->d_qjl_a;
   return run(iq::Kernel::kAttnScores, p, q_dtype, a);
+}
+
+iq_status iq_distortion_grad(const iq_params* p, int dtype, int64_t n, const void* x, double* grad, double* loss,
+                             void* stream) {
+  iq_status s = check_call(p, dtype, n);
+  if (s != IQ_OK) return s;
+  if (n == 0) return IQ_OK;
+  if (!x || !grad) return fail(IQ_ERR_INVALID_ARGUMENT, "x and grad are required");
+  if (!aligned(x, 16) || !aligned(grad, 8) || (loss && !aligned(loss, 8)))
+    return fail(IQ_ERR_MISALIGNED, "x must be 16-byte, grad and loss 8-byte aligned");
+  iq::LaunchArgs a = base_args(p, n, stream);
+  a.x = x;
+  a.grad = grad;
+  a.loss = loss;
+  return run(iq::Kernel::kDistortionGrad, p, dtype, a);
 }
 
 iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x, uint8_t* codes,

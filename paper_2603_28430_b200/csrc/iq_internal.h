@@ -75,9 +75,14 @@ IQ_HD inline uint32_t umma_sw128_off(int r, int k, int rows) {
                                ((((k % 64) / 8) ^ (r % 8)) * 16) + (k % 8) * 2);
 }
 
-// Returns false with a message on invalid input.
+// Returns false with a message on invalid input.  rot_in (nullable): explicit
+// rotation parameters in the iq_export_params layout (normalised on input)
+// instead of the seeded generator.
 bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* hp,
-                       std::string* err);
+                       std::string* err, const double* rot_in = nullptr);
+// dL/dM_b (row-major PW x PW per block) -> dL/d(rot) in the export layout,
+// projected on the tangent space of the unit sphere (R30)
+void operator_grad_to_rot(const HostParams& hp, const double* G, double* grad_rot);
 size_t rotation_param_count(int d, int variant);
 size_t block_matrix_count(int d, int variant);
 
@@ -101,6 +106,8 @@ struct LaunchArgs {
   const float* rnorms_in;
   const uint8_t* qjl_img_a;
   const uint8_t* qjl_img_rot;
+  double* grad;             // distortion gradient [block_matrix_count] (accumulated)
+  double* loss;             // distortion sum (accumulated, nullable)
   double* sums;
   void* stream;
   const uint8_t* qjl_img;   // device UMMA image of S (stage 2)
@@ -108,7 +115,7 @@ struct LaunchArgs {
   float* rnorms;            // [n] residual norms (stage 2)
 };
 
-enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5 };
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5, kDistortionGrad = 6 };
 
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.

@@ -107,6 +107,7 @@ constexpr int pick_tpl() {
   if (KIND == 3) return IQ_TPL_DEC;
 #endif
   if (KIND == 3) return (f16 && BITS == 4) ? 16 : 8;   // measured: 0.82 -> 0.89 at fp16 b = 4
+  if (KIND == 4) return 8;                               // distortion gradient (grad.cuh)
 #ifdef IQ_TPL_K3B4
   if (KIND == 1 && BITS == 4) return IQ_TPL_K3B4;
 #endif
@@ -124,7 +125,7 @@ constexpr int pick_tpl() {
 // fused kernel, and for the fp32 quantizer; registers (8 warps) otherwise.
 template <class T, int BITS, int KIND>
 constexpr bool pick_ops_smem() {
-  if (!IQ_OPS_SMEM || KIND == 3) return false;
+  if (!IQ_OPS_SMEM || KIND >= 3) return false;
   if (sizeof(T) == 2) return !(KIND == 1 && BITS <= 2);
   return KIND == 0;
 }

@@ -202,7 +202,7 @@ size_t block_matrix_count(int d, int variant) {
 }
 
 bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* hp,
-                       std::string* err) {
+                       std::string* err, const double* rot_in) {
   if (d < 1 || d > (1 << 20)) { *err = "d must be in [1, 2^20]"; return false; }
   if (bits < 1 || bits > kMaxBits) { *err = "bits must be in [1, 4]"; return false; }
   if (variant < IQ_VARIANT_FULL || variant > IQ_VARIANT_PLANAR2D) {
@@ -220,8 +220,17 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
     const uint64_t s2 = seed ^ kThetaStreamKey;
     const int g2 = (d + 1) / 2;
     for (int j = 0; j < g2; ++j) {
-      const double th = 2.0 * M_PI * unit_open0(s2, j);
-      const double c = std::cos(th), s = std::sin(th);
+      double c, s;
+      if (rot_in) {                                   // explicit (cos, sin), normalised
+        const double r = std::hypot(rot_in[2 * j], rot_in[2 * j + 1]);
+        if (!(r > 1e-12)) { *err = "explicit 2D parameters must be nonzero pairs"; return false; }
+        c = rot_in[2 * j] / r;
+        s = rot_in[2 * j + 1] / r;
+      } else {
+        const double th = 2.0 * M_PI * unit_open0(s2, j);
+        c = std::cos(th);
+        s = std::sin(th);
+      }
       hp->rot[2 * j] = c;
       hp->rot[2 * j + 1] = s;
       // R(theta) = [[c, -s], [s, c]] row-major
@@ -236,9 +245,19 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
     const bool full = variant == IQ_VARIANT_FULL;
     for (int b = 0; b < g; ++b) {
       double qL[4], qR[4] = {1.0, 0.0, 0.0, 0.0};
-      unit_quaternion(seed, 8ull * b, qL);
-      if (full) unit_quaternion(seed, 8ull * b + 4, qR);
       const int stride = full ? 8 : 4;
+      if (rot_in) {                                   // explicit quaternions u -> u / ||u||
+        for (int part = 0; part < (full ? 2 : 1); ++part) {
+          const double* u = rot_in + stride * b + 4 * part;
+          const double nu = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2] + u[3] * u[3]);
+          if (!(nu > 1e-12)) { *err = "explicit quaternions must be nonzero"; return false; }
+          double* q = part ? qR : qL;
+          for (int c = 0; c < 4; ++c) q[c] = u[c] / nu;
+        }
+      } else {
+        unit_quaternion(seed, 8ull * b, qL);
+        if (full) unit_quaternion(seed, 8ull * b + 4, qR);
+      }
       for (int c = 0; c < 4; ++c) hp->rot[stride * b + c] = qL[c];
       if (full) for (int c = 0; c < 4; ++c) hp->rot[stride * b + 4 + c] = qR[c];
       // Column j of M is T(e_j): Full q_L e_j conj(q_R), Fast q_L e_j.
@@ -286,6 +305,61 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
   }
   if (!build_grid(kc, h, err)) return false;
   return true;
+}
+
+// ------------------------------------------------------- learning (R29, R30)
+// dL/dM_b -> dL/d(rot).  Full: M = L(q_L) R(conj q_R), column j of M is
+// q_L e_j conj(q_R), so dL/dq_L[k] = sum_ij G_ij (e_k e_j conj(q_R))_i and
+// dL/dq_R[k] = sum_ij G_ij (q_L e_j conj(e_k))_i; Fast drops q_R; 2D: M =
+// [[c, -s], [s, c]].  Each unit vector's gradient is projected on the tangent
+// space (g - (g.q) q), the gradient with respect to u at ||u|| = 1.
+void operator_grad_to_rot(const HostParams& hp, const double* G, double* grad_rot) {
+  if (hp.variant == IQ_VARIANT_PLANAR2D) {
+    const int g2 = (hp.d + 1) / 2;
+    for (int j = 0; j < g2; ++j) {
+      const double* m = G + 4 * j;
+      const double c = hp.rot[2 * j], s = hp.rot[2 * j + 1];
+      const double gc = m[0] + m[3], gs = -m[1] + m[2];
+      const double dot = gc * c + gs * s;
+      grad_rot[2 * j] = gc - dot * c;
+      grad_rot[2 * j + 1] = gs - dot * s;
+    }
+    return;
+  }
+  const bool full = hp.variant == IQ_VARIANT_FULL;
+  const int stride = full ? 8 : 4;
+  const int g = (hp.d + 3) / 4;
+  for (int b = 0; b < g; ++b) {
+    const double* qL = &hp.rot[stride * b];
+    const double qR[4] = {full ? hp.rot[stride * b + 4] : 1.0, full ? hp.rot[stride * b + 5] : 0.0,
+                          full ? hp.rot[stride * b + 6] : 0.0, full ? hp.rot[stride * b + 7] : 0.0};
+    const double qRc[4] = {qR[0], -qR[1], -qR[2], -qR[3]};
+    const double* Gb = G + 16 * b;
+    double gl[4] = {0, 0, 0, 0}, gr[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k) {
+      double ek[4] = {0, 0, 0, 0};
+      ek[k] = 1.0;
+      const double ekc[4] = {ek[0], -ek[1], -ek[2], -ek[3]};
+      for (int j = 0; j < 4; ++j) {
+        double ej[4] = {0, 0, 0, 0}, t1[4], t2[4];
+        ej[j] = 1.0;
+        hamilton(ek, ej, t1);
+        hamilton(t1, qRc, t2);                               // e_k e_j conj(q_R)
+        for (int i = 0; i < 4; ++i) gl[k] += Gb[4 * i + j] * t2[i];
+        if (full) {
+          hamilton(qL, ej, t1);
+          hamilton(t1, ekc, t2);                             // q_L e_j conj(e_k)
+          for (int i = 0; i < 4; ++i) gr[k] += Gb[4 * i + j] * t2[i];
+        }
+      }
+    }
+    for (int part = 0; part < (full ? 2 : 1); ++part) {
+      const double* q = part ? qR : qL;
+      const double* gq = part ? gr : gl;
+      const double dot = gq[0] * q[0] + gq[1] * q[1] + gq[2] * q[2] + gq[3] * q[3];
+      for (int c = 0; c < 4; ++c) grad_rot[stride * b + 4 * part + c] = gq[c] - dot * q[c];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- stage 2
