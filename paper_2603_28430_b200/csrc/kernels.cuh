@@ -43,6 +43,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_OPS_SMEM
 #define IQ_OPS_SMEM 1        // large-operator encoders read their operators from shared memory
 #endif
+#ifndef IQ_PDL
+#define IQ_PDL 1             // programmatic dependent launch of the stage-1 encoders
+#endif
 #ifndef IQ_NWC_WIDE
 #define IQ_NWC_WIDE 16       // compute warps of the wide encoder CTAs
 #endif
@@ -275,6 +278,21 @@ __device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, float dep) {
       "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(bar)),
       "r"(__float_as_uint(dep))
       : "memory");
+}
+
+// Programmatic dependent launch (the launcher sets the PDL attribute): the
+// prologue (barrier setup, operator loads from the immutable parameters)
+// overlaps the previous kernel in the stream; global reads and writes of
+// the data wait for it.  Both are no-ops without the attribute.
+__device__ __forceinline__ void grid_dependency_wait() {
+#if IQ_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+#if IQ_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
@@ -711,6 +729,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 
   if (warp == NWC) {  // ---------------- producer: TMA bulk loads into the ring
     if (lane == 0) {
+      grid_dependency_wait();             // the previous kernel's writes (PDL launch)
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
@@ -723,9 +742,11 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
         bulk_g2s(smem + s * STAGE, x + v0 * D, bytes, &full[s], pol);
         if (++s == NST) { s = 0; ph ^= 1; }
       }
+      grid_launch_dependents();           // every load issued: the next kernel may launch
     }
     return;
   }
+  grid_dependency_wait();                 // before this CTA's first global write
 
   // ---------------------------------------------------- compute warps
   const int sub = lane & (G - 1);
@@ -961,6 +982,7 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
 
   if (warp == NWC) {
     if (lane == 0) {
+      grid_dependency_wait();             // the previous kernel's writes (PDL launch)
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
@@ -980,9 +1002,11 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
         }
         if (++s == NST) { s = 0; ph ^= 1; }
       }
+      grid_launch_dependents();
     }
     return;
   }
+  grid_dependency_wait();                 // before this CTA's first global access
 
   const int sub = lane & (G - 1);
   const int vslot = lane / G;

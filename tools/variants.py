@@ -24,6 +24,7 @@ VARIANTS = {
     "tchint": ["-DIQ_TC_SPIN=0"],           # suspend-hint waits on tcgen05.commit barriers
     "qjl8": ["-DIQ_QJL_NWC=8"],             # 8 compute warps in the stage-2 kernel
     "attn8": ["-DIQ_ATTN_NWD=8"],           # 8 decoder warps in the attention consumer
+    "nopdl": ["-DIQ_PDL=0"],                # no programmatic dependent launch
     "dec16": ["-DIQ_TPL_DEC=16"],           # 16 coordinates per lane in the dequantizer
     "dec4": ["-DIQ_TPL_DEC=4"],             # 4 coordinates per lane in the dequantizer
 }
