@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t tmem_sign_word16(uint32_t taddr) {
 // store fp16 hi / lo of a lane's EPC consecutive coordinates of tile row r
 // (coordinates k0 .. k0+EPC-1) into the A operand tiles
 template <int EPC>
-__device__ __forceinline__ void store_residual(uint8_t* a_hi, uint8_t* a_lo, int r, int k0, const float* rs) {
+__device__ __forceinline__ void store_residual(uint8_t* a_hi, uint8_t* a_lo, uint32_t off, const float* rs) {
   uint32_t h[EPC / 2], l[EPC / 2];
 #pragma unroll
   for (int e = 0; e < EPC; e += 2) {
@@ -140,7 +140,6 @@ __device__ __forceinline__ void store_residual(uint8_t* a_hi, uint8_t* a_lo, int
     h[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
     l[e / 2] = *reinterpret_cast<const uint32_t*>(&ll);
   }
-  const uint32_t off = umma_sw128_off(r, k0, 128);
   if constexpr (EPC == 8) {
     *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
@@ -265,7 +264,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
 
     auto epilogue = [&](uint32_t jj, int64_t tt) {
       const uint32_t b = jj & 1;
-      mbar_wait_tc(&acc_full[b], (jj >> 1) & 1);
+      mbar_wait(&acc_full[b], (jj >> 1) & 1);           // suspend-hint wait (compute warps)
       tc_fence_after();
       const int row = 32 * quad + lane;
       const int64_t v = tt * TILE + row;
@@ -419,7 +418,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         const float2 sr = mul2(rinv, bc(256.0f));
         // the previous tile's MMAs must have consumed the A tiles (the
         // stage-1 work above overlaps them)
-        if (u == 0) mbar_wait_tc(a_free, (j & 1) ^ 1);
+        if (u == 0) mbar_wait(a_free, (j & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           float ta[EPC], tb[EPC];
@@ -429,9 +428,10 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
             ta[e] = t2.x;
             tb[e] = t2.y;
           }
+          // (the offsets depend only on the lane and u: the compiler hoists them)
           const int k0 = (sub + i * G) * EPC;
-          store_residual<EPC>(a_hi, a_lo, vl, k0, ta);
-          store_residual<EPC>(a_hi, a_lo, vl + VPW, k0, tb);
+          store_residual<EPC>(a_hi, a_lo, umma_sw128_off(vl, k0, 128), ta);
+          store_residual<EPC>(a_hi, a_lo, umma_sw128_off(vl + VPW, k0, 128), tb);
         }
       }
       fence_async_smem();          // generic-proxy A writes -> tensor-core (async proxy) reads
