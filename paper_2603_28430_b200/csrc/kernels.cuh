@@ -46,6 +46,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_PDL
 #define IQ_PDL 1             // programmatic dependent launch of the stage-1 encoders
 #endif
+#ifndef IQ_NORM_SPLIT
+#define IQ_NORM_SPLIT 0      // norm as two interleaved partial sums (experiment)
+#endif
 #ifndef IQ_NWC_WIDE
 #define IQ_NWC_WIDE 16       // compute warps of the wide encoder CTAs
 #endif
@@ -801,9 +804,20 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
       for (int i = 0; i < CPL; ++i) to_pairs<T>(ra[i], rb[i], v + i * EPC);
       // Alg.1 l.1: rho = ||x||_2
+#if IQ_NORM_SPLIT
+      // two interleaved partial sums: half the dependent FFMA2 chain
+      float2 ss = mul2(v[0], v[0]), ss1 = mul2(v[1], v[1]);
+#pragma unroll
+      for (int e = 2; e < EPL; e += 2) {
+        ss = fma2(v[e], v[e], ss);
+        ss1 = fma2(v[e + 1], v[e + 1], ss1);
+      }
+      ss = add2(ss, ss1);
+#else
       float2 ss = mul2(v[0], v[0]);
 #pragma unroll
       for (int e = 1; e < EPL; ++e) ss = fma2(v[e], v[e], ss);
+#endif
       if (u + 2 == U) {                                // last rows consumed: release the stage
         __syncwarp();
         if (lane == 0) mbar_arrive_after(&empty[ss_], ss.x + ss.y);

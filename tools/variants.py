@@ -25,6 +25,7 @@ VARIANTS = {
     "qjl8": ["-DIQ_QJL_NWC=8"],             # 8 compute warps in the stage-2 kernel
     "attn8": ["-DIQ_ATTN_NWD=8"],           # 8 decoder warps in the attention consumer
     "nopdl": ["-DIQ_PDL=0"],                # no programmatic dependent launch
+    "nsplit": ["-DIQ_NORM_SPLIT=1"],        # norm as two interleaved partial sums
     "dec16": ["-DIQ_TPL_DEC=16"],           # 16 coordinates per lane in the dequantizer
     "dec4": ["-DIQ_TPL_DEC=4"],             # 4 coordinates per lane in the dequantizer
 }
