@@ -116,6 +116,27 @@ const char* iq_last_error_detail(void);
 iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device,
                          iq_params** out);
 
+/*
+ * iq_make_params_sets — n_sets independent rotation sets in one handle
+ * (per-(layer, head) parameters; R31): set s
+ * is what iq_make_params builds from seed + s; the codebook is shared.  Rows
+ * are laid out set-major: row r of any call uses set (r / set_rows) %
+ * n_sets (a KV cache [layers, heads, tokens, d] with set_rows = tokens gives
+ * one set per (layer, head)); iq_attention_scores uses set h % n_sets for
+ * head h.  set_rows must be a positive multiple of 256 (tiles never straddle
+ * sets).  Supported by iq_quantize / iq_dequantize / iq_roundtrip / the host
+ * pipeline and iq_attention_scores; not by the stage-2 sketch or the
+ * distortion gradient (UNSUPPORTED / no sketch).
+ */
+iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows,
+                              int device, iq_params** out);
+
+/* n_sets and set_rows of a handle (1 and 0 for a single-set handle). */
+iq_status iq_params_sets_info(const iq_params* p, int* n_sets, int64_t* set_rows);
+
+/* Rotation parameters of one set (iq_export_params exports set 0). */
+iq_status iq_export_params_set(const iq_params* p, int set, double* rot, size_t rot_len);
+
 /* Release a handle (NULL is a no-op).  The caller guarantees no kernel that
  * uses it is still in flight. */
 iq_status iq_free_params(iq_params* p);

@@ -24,6 +24,7 @@ __all__ = [
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
     "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
     "iq_attention_scores", "iq_make_params_explicit", "iq_distortion_grad", "iq_rot_grad_from_operator_grad",
+    "iq_make_params_sets", "iq_export_params_set",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -67,6 +68,9 @@ _sig = {
     "iq_make_params_explicit": (_c_int, [_c_int, _c_int, _c_int, _c_vp, _c_sz, _c_int, ctypes.POINTER(_c_vp)]),
     "iq_distortion_grad": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "iq_rot_grad_from_operator_grad": (_c_int, [_c_vp, _c_vp, _c_sz, _c_vp, _c_sz]),
+    "iq_make_params_sets": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_vp)]),
+    "iq_params_sets_info": (_c_int, [_c_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_c_i64)]),
+    "iq_export_params_set": (_c_int, [_c_vp, _c_int, _c_vp, _c_sz]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -156,6 +160,23 @@ def iq_export_qjl_matrix(p: Params) -> np.ndarray:
     S = np.zeros((p.d, p.d), dtype=np.float32)
     _check(lib.iq_export_qjl_matrix(p.handle, S.ctypes.data, S.size), "iq_export_qjl_matrix")
     return S
+
+
+def iq_make_params_sets(d: int, bits: int, variant, seed: int, n_sets: int, set_rows: int, device: int = 0) -> Params:
+    """n_sets rotation sets (set s = the seed + s parameters); row r uses set
+    (r // set_rows) % n_sets, head h of the consumer set h % n_sets."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant.lower()]
+    h = ctypes.c_void_p()
+    _check(lib.iq_make_params_sets(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
+                                   int(n_sets), int(set_rows), int(device), ctypes.byref(h)), "iq_make_params_sets")
+    return Params(h.value, d, bits, variant, seed, device)
+
+
+def iq_export_params_set(p: Params, s: int) -> np.ndarray:
+    rot = np.zeros(iq_rotation_param_count(p.d, p.variant), dtype=np.float64)
+    _check(lib.iq_export_params_set(p.handle, int(s), rot.ctypes.data, rot.size), "iq_export_params_set")
+    return rot
 
 
 def iq_make_params_explicit(d: int, bits: int, variant, rot, device: int = 0) -> Params:

@@ -259,6 +259,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     // S q (stage 2), fp16 with per-query power-of-two scales
     auto load_queries = [&](int64_t h) {
       const TQ* qh = q + h * (int64_t)n_q * D;
+      const float* mset = mat + (size_t)(h % cb.n_sets) * cb.set_stride;   // the head's set [R31]
       if (st2 && threadIdx.x == 0) {             // stage S in the drained A buffers
         mbar_arrive_expect_tx(s_bar, A::S_BYTES);
         bulk_g2s(a_base, s_img, A::S_BYTES, s_bar, policy_evict_last());
@@ -291,7 +292,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         for (int r = 0; r < PW; ++r) {
           float a = 0.0f;
 #pragma unroll
-          for (int c = 0; c < PW; ++c) a = fmaf(__ldg(mat + (size_t)b * PW * PW + r * PW + c), xv[c], a);
+          for (int c = 0; c < PW; ++c) a = fmaf(__ldg(mset + (size_t)b * PW * PW + r * PW + c), xv[c], a);
           yv[r] = a;
         }
 #pragma unroll

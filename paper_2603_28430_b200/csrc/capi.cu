@@ -126,7 +126,8 @@ const char* iq_status_string(iq_status s) {
 const char* iq_last_error_detail(void) { return g_detail.c_str(); }
 
 static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, int device, bool qjl,
-                                  iq_params** out, const double* rot_in = nullptr) {
+                                  iq_params** out, const double* rot_in = nullptr, int n_sets = 1,
+                                  int64_t set_rows = 0) {
   if (!out) return fail(IQ_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (device < -1) return fail(IQ_ERR_INVALID_ARGUMENT, "device must be >= -1");
@@ -134,7 +135,7 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
   if (!p) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
   std::string err;
   if (!iq::build_host_params(d, bits, variant, seed, &p->hp, &err, rot_in) ||
-      (qjl && !iq::build_qjl(&p->hp, &err))) {
+      (qjl && !iq::build_qjl(&p->hp, &err)) || (n_sets > 1 && !iq::add_param_sets(&p->hp, n_sets, set_rows, &err))) {
     delete p;
     return fail(IQ_ERR_INVALID_ARGUMENT, err);
   }
@@ -186,6 +187,30 @@ iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int de
   return make_params_impl(d, bits, variant, seed, device, true, out);
 }
 
+iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows, int device,
+                              iq_params** out) {
+  if (n_sets < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "n_sets must be >= 1");
+  if (n_sets > 1 && (set_rows < 256 || set_rows % 256 != 0))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "set_rows must be a positive multiple of 256");
+  return make_params_impl(d, bits, variant, seed, device, false, out, nullptr, n_sets, set_rows);
+}
+
+iq_status iq_params_sets_info(const iq_params* p, int* n_sets, int64_t* set_rows) {
+  if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
+  if (n_sets) *n_sets = p->hp.n_sets;
+  if (set_rows) *set_rows = p->hp.set_rows;
+  return IQ_OK;
+}
+
+iq_status iq_export_params_set(const iq_params* p, int set, double* rot, size_t rot_len) {
+  if (!p || !rot) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (set < 0 || set >= p->hp.n_sets) return fail(IQ_ERR_INVALID_ARGUMENT, "set out of range");
+  const size_t nr = iq::rotation_param_count(p->hp.d, p->hp.variant);
+  if (rot_len < nr) return fail(IQ_ERR_BUFFER_TOO_SMALL, "rot buffer too small");
+  std::memcpy(rot, p->hp.rot.data() + (size_t)set * nr, nr * sizeof(double));
+  return IQ_OK;
+}
+
 iq_status iq_make_params_explicit(int d, int bits, int variant, const double* rot, size_t rot_len, int device,
                                   iq_params** out) {
   if (!rot) return fail(IQ_ERR_INVALID_ARGUMENT, "rot is NULL");
@@ -197,6 +222,7 @@ iq_status iq_make_params_explicit(int d, int bits, int variant, const double* ro
 iq_status iq_rot_grad_from_operator_grad(const iq_params* p, const double* G, size_t G_len, double* grad_rot,
                                          size_t rot_len) {
   if (!p || !G || !grad_rot) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (p->hp.n_sets > 1) return fail(IQ_ERR_UNSUPPORTED, "single-set handles only");
   if (G_len < p->hp.mat.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "G shorter than the block operators");
   if (rot_len < p->hp.rot.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "grad_rot shorter than the rotation params");
   iq::operator_grad_to_rot(p->hp, G, grad_rot);
@@ -242,9 +268,10 @@ iq_status iq_export_params(const iq_params* p, double* rot, size_t rot_len, floa
                            size_t centroids_len, float* thresholds, size_t thresholds_len) {
   if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
   const auto& hp = p->hp;
-  if (rot) {
-    if (rot_len < hp.rot.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "rot buffer too small");
-    std::memcpy(rot, hp.rot.data(), hp.rot.size() * sizeof(double));
+  if (rot) {                                  // set 0 (iq_export_params_set for the others)
+    const size_t nr = iq::rotation_param_count(hp.d, hp.variant);
+    if (rot_len < nr) return fail(IQ_ERR_BUFFER_TOO_SMALL, "rot buffer too small");
+    std::memcpy(rot, hp.rot.data(), nr * sizeof(double));
   }
   if (centroids) {
     if (centroids_len < hp.centroids.size())
@@ -261,8 +288,9 @@ iq_status iq_export_params(const iq_params* p, double* rot, size_t rot_len, floa
 
 iq_status iq_export_block_matrices(const iq_params* p, float* m, size_t m_len) {
   if (!p || !m) return fail(IQ_ERR_INVALID_ARGUMENT, "NULL argument");
-  if (m_len < p->hp.mat.size()) return fail(IQ_ERR_BUFFER_TOO_SMALL, "matrix buffer too small");
-  std::memcpy(m, p->hp.mat.data(), p->hp.mat.size() * sizeof(float));
+  const size_t nm = iq::block_matrix_count(p->hp.d, p->hp.variant);   // set 0
+  if (m_len < nm) return fail(IQ_ERR_BUFFER_TOO_SMALL, "matrix buffer too small");
+  std::memcpy(m, p->hp.mat.data(), nm * sizeof(float));
   return IQ_OK;
 }
 
@@ -345,6 +373,7 @@ iq_status iq_distortion_grad(const iq_params* p, int dtype, int64_t n, const voi
                              void* stream) {
   iq_status s = check_call(p, dtype, n);
   if (s != IQ_OK) return s;
+  if (p->hp.n_sets > 1) return fail(IQ_ERR_UNSUPPORTED, "the distortion gradient takes a single-set handle");
   if (n == 0) return IQ_OK;
   if (!x || !grad) return fail(IQ_ERR_INVALID_ARGUMENT, "x and grad are required");
   if (!aligned(x, 16) || !aligned(grad, 8) || (loss && !aligned(loss, 8)))
@@ -472,6 +501,8 @@ iq_status iq_host_pipeline_create(const iq_params* p, int dtype, int64_t chunk_v
   iq_status s = check_call(p, dtype, 0);
   if (s != IQ_OK) return s;
   if (chunk_vectors <= 0) return fail(IQ_ERR_INVALID_ARGUMENT, "chunk_vectors must be > 0");
+  if (p->hp.n_sets > 1 && chunk_vectors % (p->hp.set_rows * p->hp.n_sets) != 0)
+    return fail(IQ_ERR_INVALID_ARGUMENT, "with parameter sets, chunk_vectors must be a multiple of set_rows * n_sets");
   iq_host_pipeline* pl = new (std::nothrow) iq_host_pipeline();
   if (!pl) return fail(IQ_ERR_OUT_OF_MEMORY, "host allocation failed");
   pl->p = p;

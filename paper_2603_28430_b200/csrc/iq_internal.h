@@ -35,6 +35,11 @@ struct KCodebook {
   float gtab[32];              // [j] = nextdown(tau * S) of the threshold in cell j (else +inf);
                                // [16 + j] = cpos[m_start(j)]
   uint32_t gcode[32];          // [16 + j] = m_start(j) | h  (code magnitude, sign added later)
+  // Parameter sets (R31): row r uses the operators of set
+  // (r / set_rows) % n_sets, at mat + set * set_stride; n_sets = 1: one set.
+  int64_t set_rows;
+  int32_t n_sets;
+  int32_t set_stride;
 };
 
 // Host-side parameter construction (params.cpp): the reference generator of
@@ -42,6 +47,8 @@ struct KCodebook {
 struct HostParams {
   int d = 0, bits = 0, variant = 0;
   uint64_t seed = 0;
+  int n_sets = 1;                  // parameter sets (R31): rot / mat hold n_sets copies
+  int64_t set_rows = 0;
   std::vector<double> rot;        // canonical fp64 (see iq_export_params)
   std::vector<float> mat;         // device operator, fp32 (see iq_export_block_matrices)
   std::vector<float> centroids;   // [L] fp32 ascending
@@ -59,6 +66,10 @@ struct HostParams {
   // lo parts (S' to ~2^-22), two K-major 128B-swizzled B images back to back
   std::vector<uint8_t> qjl_img_rot;
 };
+
+// n_sets - 1 further rotation sets (set s from seed + s, R31) appended to
+// rot / mat; set_rows rows per set.
+bool add_param_sets(HostParams* hp, int n_sets, int64_t set_rows, std::string* err);
 
 // Sketch generator key and layout (params.cpp).
 bool build_qjl(HostParams* hp, std::string* err);

@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "iq_internal.h"
 
 namespace iq {
@@ -694,6 +696,45 @@ __device__ __forceinline__ void fetch_op(const float (&P)[Gm::OPS_SMEM ? 1 : Gm:
   }
 }
 
+// Parameter sets (R31): reload the lane's operators when the tile's set
+// differs from the loaded one.  Every compute warp walks the same tiles, so
+// the branch is CTA-uniform; shared-memory operators are rewritten between
+// two compute-warp barriers.  Tiles never straddle sets (set_rows is a
+// multiple of 256, every TILE_V divides 256).
+// Rewrite the shared-memory operators of a CTA with those of `ms`, one
+// float4 at a time (rolled loops: it runs only at a set change and must not
+// add register pressure to the hot loop).
+template <class Gm>
+__device__ __forceinline__ void reload_ops_smem(const float* __restrict__ ms, int sub, uint8_t* ops) {
+  constexpr int PW = Gm::PW, EPC = Gm::EPC, G = Gm::G, NPB = PW * PW, NQ = NPB / 4;
+#pragma unroll 1
+  for (int b = 0; b < Gm::NBL; ++b) {
+    const int lc = b * PW;
+    const int gc = (sub + (lc / EPC) * G) * EPC + lc % EPC;
+    const float4* m = reinterpret_cast<const float4*>(ms + (size_t)(gc / PW) * NPB);
+#pragma unroll 1
+    for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(ops)[(b * NQ + q) * G + sub] = __ldg(m + q);
+  }
+}
+
+template <class Gm, int NWC_BAR = Gm::NWC>
+__device__ __forceinline__ void switch_ops(const float* __restrict__ mat, const KCodebook& cb, int64_t v0,
+                                           int& cur_set, int sub, int warp, int lane, uint8_t* ops,
+                                           float (&P)[Gm::OPS_SMEM ? 1 : Gm::NBL][Gm::PW * Gm::PW]) {
+  if (cb.n_sets <= 1) return;
+  const int set = (int)((v0 / cb.set_rows) % cb.n_sets);
+  if (set == cur_set) return;
+  cur_set = set;
+  const float* ms = mat + (size_t)set * cb.set_stride;
+  if constexpr (Gm::OPS_SMEM) {
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC_BAR * 32) : "memory");   // old operators no longer read
+    if (warp == 0 && lane < Gm::G) reload_ops_smem<Gm>(ms, sub, ops);
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC_BAR * 32) : "memory");
+  } else {
+    load_ops<Gm>(ms, sub, P);
+  }
+}
+
 // Ring setup shared by the three kernels.
 template <int NST, int NWC>
 __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
@@ -709,7 +750,7 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
 // --------------------------------------------------------- encoder (K1/K3)
 // MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y only).
 // MODE 2: fused roundtrip that also writes codes and norms.
-template <class T, int D, int BITS, int VAR, int MODE>
+template <class T, int D, int BITS, int VAR, int MODE, bool SETS = false>
 __global__ void __launch_bounds__(Geo<T, D, BITS, VAR, MODE>::CTA_THREADS,
                                   Geo<T, D, BITS, VAR, MODE>::MIN_CTAS)
 k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x, T* y,
@@ -776,7 +817,9 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 
   int s = 0;
   uint32_t ph = 0;
+  int cur_set = 0;                                       // operators of set 0 are loaded
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if constexpr (SETS) switch_ops<Gm>(mat, cb, t * TILE_V, cur_set, sub, warp, lane, ops, P);   // [R31]
     mbar_wait_warp(&full[s], ph, lane);
     const uint8_t* st = smem + s * STAGE;
     const int ss_ = s;
@@ -972,7 +1015,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 // centroid lookup C[code] is a warp shuffle from a register table
 // (lane k of every aligned group of L lanes holds C[k]); the shuffle's
 // width-L source index does the masking of the code field.
-template <class T, int D, int BITS, int VAR>
+template <class T, int D, int BITS, int VAR, bool SETS = false>
 __global__ void __launch_bounds__(Geo<T, D, BITS, VAR, 3>::CTA_THREADS,
                                   Geo<T, D, BITS, VAR, 3>::MIN_CTAS)
 k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
@@ -1030,7 +1073,9 @@ k_decode(const float* __restrict__ mat, const KCodebook cb, int64_t n,
 
   int s = 0;
   uint32_t ph = 0;
+  int cur_set = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if constexpr (SETS) switch_ops<Gm>(mat, cb, t * TILE_V, cur_set, sub, warp, lane, nullptr, P);   // [R31]
     mbar_wait_warp(&full[s], ph, lane);
     const uint8_t* st = smem + s * STAGE;
     const int64_t v0 = t * TILE_V;

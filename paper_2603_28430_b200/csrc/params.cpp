@@ -284,6 +284,9 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
         (static_cast<double>(hp->centroids[k]) + static_cast<double>(hp->centroids[k + 1])) * 0.5);
   KCodebook& kc = hp->kcb;
   std::memset(&kc, 0, sizeof kc);
+  kc.n_sets = 1;
+  kc.set_rows = 0;
+  kc.set_stride = static_cast<int32_t>(hp->mat.size());
   for (int m = 0; m < h; ++m) kc.cpos[m] = hp->centroids[h + m];
   for (int m = 1; m < h; ++m) kc.tau[m] = hp->thresholds[h - 1 + m];
   for (int m = 0; m < kMaxHalf; ++m) std::memcpy(&kc.tau_bits[m], &kc.tau[m], 4);
@@ -304,6 +307,26 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
     kc.delta[m] = dlt;
   }
   if (!build_grid(kc, h, err)) return false;
+  return true;
+}
+
+// ------------------------------------------------------------ sets (R31)
+bool add_param_sets(HostParams* hp, int n_sets, int64_t set_rows, std::string* err) {
+  if (n_sets < 1) { *err = "n_sets must be >= 1"; return false; }
+  const size_t nrot = hp->rot.size(), nmat = hp->mat.size();
+  for (int s = 1; s < n_sets; ++s) {
+    HostParams t;
+    if (!build_host_params(hp->d, hp->bits, hp->variant, hp->seed + static_cast<uint64_t>(s), &t, err))
+      return false;
+    hp->rot.insert(hp->rot.end(), t.rot.begin(), t.rot.end());
+    hp->mat.insert(hp->mat.end(), t.mat.begin(), t.mat.end());
+  }
+  hp->n_sets = n_sets;
+  hp->set_rows = set_rows;
+  hp->kcb.n_sets = n_sets;
+  hp->kcb.set_rows = set_rows;
+  hp->kcb.set_stride = static_cast<int32_t>(nmat);
+  (void)nrot;
   return true;
 }
 

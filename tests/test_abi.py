@@ -140,3 +140,18 @@ def test_qjl_sketch_generator_matches_oracle(iq):
     p = iq.iq_make_params(64, 3, iq.FULL, 1, device=-1)
     with pytest.raises(iq.IQError):
         iq.iq_export_qjl_matrix(p)
+
+
+def test_param_sets_generator_matches_oracle(iq):
+    """Set s of a multi-set handle is exactly the seed + s parameters (R31)."""
+    from oracle import iq_oracle as O
+    p = iq.iq_make_params_sets(64, 3, iq.FULL, 20260331, 3, 256, device=-1)
+    for s in range(3):
+        want = iq.iq_export_params(iq.iq_make_params(64, 3, iq.FULL, 20260331 + s, device=-1))["rot"]
+        assert np.array_equal(iq.iq_export_params_set(p, s), want)
+        qL, qR, _ = O.make_rotation_params(64, O.FULL, 20260331 + s)
+        assert np.allclose(want.reshape(-1, 8)[:, :4], qL, atol=1e-15)
+    with pytest.raises(iq.IQError):
+        iq.iq_make_params_sets(64, 3, iq.FULL, 1, 2, 100, device=-1)     # set_rows % 256 != 0
+    with pytest.raises(iq.IQError):
+        iq.iq_export_params_set(p, 3)
