@@ -219,14 +219,20 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const float* side = reinterpret_cast<const float*>(smem + A::SIDE_OFF + c * A::SIDE_BYTES);
       const int64_t k = k0 + row;
       if (k < n_keys) {
-        const float rho = side[row], gam = side[TILE + row];
+        const float rho = side[row], gam = side[TILE + row], cg = cpi * gam;
         float* out = scores + h * (int64_t)n_q * n_keys + k;
+        // query slots in groups of four; n_q is uniform, so the early exit
+        // leaves no per-slot branches
 #pragma unroll
-        for (int jq = 0; jq < NQ; ++jq) {
-          if (jq < n_q) {
+        for (int g4 = 0; g4 < NQ / 4; ++g4) {
+          if (4 * g4 >= n_q) break;
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int jq = 4 * g4 + c4;
             float sv = __uint_as_float(v1[jq]) * side[2 * TILE + jq] * rho;
-            if (st2) sv = fmaf(__uint_as_float(v2[jq]) * side[2 * TILE + NQ + jq], cpi * gam, sv);
-            __stcs(out + (int64_t)jq * n_keys, sv);
+            if (st2) sv = fmaf(__uint_as_float(v2[jq]) * side[2 * TILE + NQ + jq], cg, sv);
+            if (jq < n_q) __stcs(out, sv);
+            out += n_keys;
           }
         }
       }
