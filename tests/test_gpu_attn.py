@@ -107,3 +107,40 @@ def test_attn_errors():
     codes6 = torch.zeros((2, 6, 48), dtype=torch.uint8, device="cuda")
     with pytest.raises(iq.IQError):
         iq.iq_attention_scores(p, codes6, norms[:, :6].contiguous(), q[:, :4].contiguous())   # 6 % 4 != 0
+
+
+def test_attn_kv_cache_shaped_sample():
+    """configs[2] shape (32 layers x 8 KV heads x 32768 tokens, Fast d=128
+    b=4 fp16, 4 queries per KV head) in one launch with the stage-2 sketch;
+    sampled heads and keys against the oracle."""
+    d, bits, heads, n_keys = 128, 4, 32 * 8, 32768
+    p = iq.iq_make_params_qjl(d, bits, iq.FAST, SEED, device=0)
+    n = heads * n_keys
+    codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device="cuda")
+    norms = torch.empty(n, dtype=torch.float32, device="cuda")
+    qj = torch.empty((n, d // 8), dtype=torch.uint8, device="cuda")
+    rn = torch.empty(n, dtype=torch.float32, device="cuda")
+    chunk = 1 << 22
+    for r0 in range(0, n, chunk):
+        x = iqsynth.device_unit_vectors(chunk, d, 600 + r0 // chunk, torch.float16, "cuda")
+        iq.iq_quantize_qjl(p, x, codes[r0:r0 + chunk], norms[r0:r0 + chunk], qj[r0:r0 + chunk], rn[r0:r0 + chunk])
+    del x
+    q = torch.randn((heads, 4, d), dtype=torch.float16, device="cuda")
+    sc = iq.iq_attention_scores(p, codes.view(heads, n_keys, -1), norms.view(heads, n_keys), q,
+                                qj.view(heads, n_keys, -1), rn.view(heads, n_keys))
+    torch.cuda.synchronize()
+    po = O.make_params(d, bits, iq.FAST, SEED)
+    S = Q.sketch_matrix(d, SEED)
+    rng = np.random.default_rng(2)
+    for h in (0, 137, heads - 1):
+        ks = np.sort(rng.choice(n_keys, 512, replace=False))
+        rows = torch.from_numpy(h * n_keys + ks).cuda()
+        cu = O.unpack_codes(codes[rows].cpu().numpy(), bits, d)
+        g = rn[rows].cpu().numpy().astype(np.float64)
+        nn = norms[rows].cpu().numpy().astype(np.float64)
+        Qf = q[h].float().cpu().numpy().astype(np.float64)
+        want = A.attention_scores(Qf, cu, nn, po, Q.unpack_bits(qj[rows].cpu().numpy(), d), g, S)
+        got = sc[h][:, torch.from_numpy(ks).cuda()].cpu().numpy()
+        qn = np.linalg.norm(Qf, axis=1)[:, None]
+        tol = 2e-3 * nn[None, :] * qn + 2e-3 * np.sqrt(d) * g[None, :] * qn
+        assert np.all(np.abs(got - want) <= tol)
