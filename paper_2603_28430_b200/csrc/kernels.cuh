@@ -48,6 +48,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_PDL
 #define IQ_PDL 1             // programmatic dependent launch of the stage-1 encoders
 #endif
+#ifndef IQ_RING_WIDE_KB
+#define IQ_RING_WIDE_KB 128  // TMA ring of the 16-warp encoders (measured: 128 KB > 200 KB, ~1-2%)
+#endif
+#ifndef IQ_STORE_CS
+#define IQ_STORE_CS 1        // streaming (evict-first) 128-bit output stores
+#endif
 #ifndef IQ_NORM_SPLIT
 #define IQ_NORM_SPLIT 0      // norm as two interleaved partial sums (experiment)
 #endif
@@ -159,7 +165,7 @@ struct Geo {
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
   static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
   static constexpr int OPS_BYTES = OPS_SMEM ? G * NBL * PW * PW * 4 : 0;
-  static constexpr int RING = WIDE ? 200 * 1024 - OPS_BYTES : IQ_RING_KB * 1024;   // TMA ring per CTA
+  static constexpr int RING = WIDE ? IQ_RING_WIDE_KB * 1024 - OPS_BYTES : IQ_RING_KB * 1024;   // TMA ring per CTA
   static constexpr int ROWB = D * (int)sizeof(T);                  // bytes per row of x
   static constexpr int RB = D * BITS / 8;                          // code bytes per row
   static constexpr int B = EPC * BITS;                             // code bits per chunk
@@ -347,7 +353,11 @@ __device__ __forceinline__ float ldsf(const void* p) {
   return r;
 }
 __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+#if IQ_STORE_CS
   __stcs(reinterpret_cast<uint4*>(p), v);
+#else
+  *reinterpret_cast<uint4*>(p) = v;
+#endif
 }
 // MUFU square root / reciprocal square root, flush-to-zero (no denormal
 // fix-up code): the norm of a row with ||x||^2 < 2^-126 is flushed.

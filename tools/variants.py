@@ -26,6 +26,11 @@ VARIANTS = {
     "attn8": ["-DIQ_ATTN_NWD=8"],           # 8 decoder warps in the attention consumer
     "nopdl": ["-DIQ_PDL=0"],                # no programmatic dependent launch
     "nsplit": ["-DIQ_NORM_SPLIT=1"],        # norm as two interleaved partial sums
+    "ring128": ["-DIQ_RING_WIDE_KB=128"],   # smaller TMA ring in the wide encoders
+    "ring96": ["-DIQ_RING_WIDE_KB=96"],
+    "ring112": ["-DIQ_RING_WIDE_KB=112"],
+    "ring160": ["-DIQ_RING_WIDE_KB=160"],
+    "stwb": ["-DIQ_STORE_CS=0"],            # ordinary (write-back) output stores
     "dec16": ["-DIQ_TPL_DEC=16"],           # 16 coordinates per lane in the dequantizer
     "dec4": ["-DIQ_TPL_DEC=4"],             # 4 coordinates per lane in the dequantizer
 }
