@@ -106,7 +106,7 @@ iq_status run(iq::Kernel k, const iq_params* p, int dtype, const iq::LaunchArgs&
 
 extern "C" {
 
-const char* iq_version(void) { return "isoquant-b200 0.1.0 (sm_100a)"; }
+const char* iq_version(void) { return "isoquant-b200 0.2.0 (sm_100a)"; }
 int iq_abi_version(void) { return IQ_ABI_VERSION; }
 
 const char* iq_status_string(iq_status s) {

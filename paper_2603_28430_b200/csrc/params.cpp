@@ -313,7 +313,7 @@ bool build_host_params(int d, int bits, int variant, uint64_t seed, HostParams* 
 // ------------------------------------------------------------ sets (R31)
 bool add_param_sets(HostParams* hp, int n_sets, int64_t set_rows, std::string* err) {
   if (n_sets < 1) { *err = "n_sets must be >= 1"; return false; }
-  const size_t nrot = hp->rot.size(), nmat = hp->mat.size();
+  const size_t nmat = hp->mat.size();
   for (int s = 1; s < n_sets; ++s) {
     HostParams t;
     if (!build_host_params(hp->d, hp->bits, hp->variant, hp->seed + static_cast<uint64_t>(s), &t, err))
@@ -326,7 +326,6 @@ bool add_param_sets(HostParams* hp, int n_sets, int64_t set_rows, std::string* e
   hp->kcb.n_sets = n_sets;
   hp->kcb.set_rows = set_rows;
   hp->kcb.set_stride = static_cast<int32_t>(nmat);
-  (void)nrot;
   return true;
 }
 
