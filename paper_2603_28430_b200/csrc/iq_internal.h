@@ -24,17 +24,17 @@ struct KCodebook {
   float delta[kMaxHalf];       // delta[m] m>=1: fp32 step with fl(cpos[m-1] + delta[m])
                                // == cpos[m] exactly, so an FMA chain over the
                                // decision indicators lands exactly on C[code]
-  // Uniform-grid decision tables (reading R19).  u = |ybar| * gscale
-  // (gscale a power of two, so u is ybar scaled exactly) falls in cell
+  // Uniform-grid decision tables (reading R19).  u = |T x| * S /
+  // max(rho, eps) (gscale S a power of two, formed inside FFMA) falls in cell
   // j = min(floor(u), NC - 1); each cell holds at most one positive threshold,
-  // so the magnitude code is m_start(j) + [u >= gtab[j]] and, because the
-  // upper part of cell j has the code of the start of cell j + 1, the lookup
-  // index is j + [u >= gtab[j]] into lanes 16..31.
+  // so the magnitude code is m_start(j) + [u > nextdown(tau S)] and, because
+  // the upper part of cell j has the code of the start of cell j + 1, the
+  // value / code lookup index is j + that increment.
   float gscale;                // S = 2^k
   uint32_t gclamp;             // bit pattern of 2^23 + (NC - 1)
-  float gtab[32];              // [j] = nextdown(tau * S) of the threshold in cell j (else +inf);
-                               // [16 + j] = cpos[m_start(j)]
-  uint32_t gcode[32];          // [16 + j] = m_start(j) | h  (code magnitude, sign added later)
+  float gtab[32];              // [j] = nextdown(tau * S) of the threshold in cell j (else +inf)
+  float gval[32];              // [j] = cpos[m_start(j)]
+  uint32_t gcode[32];          // [j] = m_start(j) | h  (code magnitude, sign added later)
   // Parameter sets (R31): row r uses the operators of set
   // (r / set_rows) % n_sets, at mat + set * set_stride; n_sets = 1: one set.
   int64_t set_rows;

@@ -596,27 +596,31 @@ __device__ __forceinline__ void encode_chunk(const float2* y, const RowQ<BITS>& 
 }
 
 // Uniform-grid decision (reading R19, tables built in params.cpp): u =
-// |ybar| * S with S = 2^k (the caller folds S into the normalisation, so u is
-// exactly the scaled rotated coordinate).  Cell j = min(floor(u), NC - 1)
-// (FADD.RM against 2^23 puts floor(u) in the low mantissa bits), one SHFL
-// fetches the cell's threshold, and the index j + 16 + [u >= threshold]
-// selects the magnitude entry; the shuffles read only the index's low five
-// bits.  Per coordinate: FADD, IMNMX, SHFL, FADD, LEA.HI -- independent of the
-// number of thresholds (7 at b = 4).
-__device__ __forceinline__ uint32_t grid_index(float y, float gtab, uint32_t gclamp) {
-  const float au = fabsf(y);
-  uint32_t t = __float_as_uint(__fadd_rd(au, 8388608.0f));
+// |y| * sc with y = T(x) unnormalised and sc = S / max(rho, eps), S = 2^k,
+// formed inside the FFMAs (no separate scaling pass).  Cell j =
+// min(floor(u), NC - 1) (FFMA.RM against 2^23 puts floor(u) in the low
+// mantissa bits), one SHFL fetches the cell's threshold, and the index
+// j + [u > nextdown(threshold)] selects the magnitude entry of gval / gcode;
+// the shuffles read only the index's low five bits.  Per coordinate: FFMA.RM,
+// IMNMX, SHFL, FFMA, LEA.HI -- independent of the number of thresholds (7 at
+// b = 4).
+__device__ __forceinline__ uint32_t grid_index(float y, float sc, float gtab, uint32_t gclamp) {
+  uint32_t t = __float_as_uint(__fmaf_rd(fabsf(y), sc, 8388608.0f));
   t = min(t, gclamp);
-  // the table holds nextdown(threshold): u >= threshold <=> nextdown - u < 0,
-  // and the sign bit of that difference is the increment (ties go up [R3])
-  const float dlt = __shfl_sync(kFull, gtab, (int)t) - au;
-  return t + 16u + (__float_as_uint(dlt) >> 31);
+  // the table holds nextdown(threshold): u >= threshold <=> nextdown - u < 0
+  // on fp32 u, and the sign bit of that difference is the increment [R3, R19]
+  const float dlt = __fmaf_rn(-fabsf(y), sc, __shfl_sync(kFull, gtab, (int)t));
+  return t + (__float_as_uint(dlt) >> 31);
 }
 // signed code of a grid index: (m | h) for ybar >= 0, h - 1 - m = (m | h) ^ (2h - 1) below
 template <int BITS>
 __device__ __forceinline__ uint32_t grid_code(uint32_t idx, float y, uint32_t gcode) {
   const uint32_t mh = (uint32_t)__shfl_sync(kFull, (int)gcode, (int)idx);
   return mh ^ ((uint32_t)((int)__float_as_uint(y) >> 31) & ((1u << BITS) - 1u));
+}
+// signed centroid of a grid index (C[code], unscaled)
+__device__ __forceinline__ float grid_value(uint32_t idx, float y, float gval) {
+  return sign_xor(__shfl_sync(kFull, gval, (int)idx), y);
 }
 
 // ------------------------------------------------------------- bit packing
@@ -823,6 +827,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   const float ctab = cb.cent[lane & ((1 << BITS) - 1)];   // C[k] in lane k of each group of L
   constexpr bool GRID = BITS >= IQ_GRID_MIN_BITS;          // uniform-grid decision [R19]
   const float gtab = cb.gtab[lane];
+  const float gval = cb.gval[lane];
   const uint32_t gcode = cb.gcode[lane];
 
   int s = 0;
@@ -884,30 +889,27 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
 #pragma unroll
       for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
       if constexpr (GRID) {
-        // ybar * S = T(x * S / max(rho, eps)): one exact power-of-two scaling
-        // folded into the normalisation (Alg.1 l.1) [R19]
+        // u = |T x| * S / max(rho, eps): the normalisation (Alg.1 l.1) and
+        // the power-of-two grid scale enter as the FFMAs' multiplier [R19]
         const float2 sc = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)) * cb.gscale,
                              rsqrt_ftz(fmaxf(ss.y, 1e-24f)) * cb.gscale);
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) v[e] = mul2(v[e], sc);
 #pragma unroll
         for (int b = 0; b < NBL; ++b) {
           float2 yb[PW], cq[PW];
           float Mb[PW * PW];
           fetch_op<Gm>(P, ops, sub, b, Mb);
-          rot_fwd<PW>(Mb, v + b * PW, yb);               // S * T(xbar)  (Alg.1 l.5/9/13)
+          rot_fwd<PW>(Mb, v + b * PW, yb);               // T(x)  (Alg.1 l.5/9/13)
 #pragma unroll
           for (int j = 0; j < PW; ++j) {
-            const uint32_t ia = grid_index(yb[j].x, gtab, cb.gclamp);
-            const uint32_t ib = grid_index(yb[j].y, gtab, cb.gclamp);
+            const uint32_t ia = grid_index(yb[j].x, sc.x, gtab, cb.gclamp);
+            const uint32_t ib = grid_index(yb[j].y, sc.y, gtab, cb.gclamp);
             if constexpr (emit) {
               const int e = (b * PW + j) % EPC, c = (b * PW + j) / EPC;
               cwa[c] |= grid_code<BITS>(ia, yb[j].x, gcode) << (e * BITS);
               cwb[c] |= grid_code<BITS>(ib, yb[j].y, gcode) << (e * BITS);
             }
             if constexpr (value)                         // v^ = C[code] (sign restored)
-              cq[j] = f2(sign_xor(__shfl_sync(kFull, gtab, (int)ia), yb[j].x),
-                         sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[j].y));
+              cq[j] = f2(grid_value(ia, yb[j].x, gval), grid_value(ib, yb[j].y, gval));
           }
           if constexpr (value) {
             rot_inv<PW>(Mb, cq, out + b * PW);           // T^-1 (l.7/11/15)

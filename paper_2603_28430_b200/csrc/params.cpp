@@ -153,9 +153,11 @@ bool build_grid(KCodebook& kc, int h, std::string* err) {
       if (cell[m] < j) ++mstart;
     }
     kc.gtab[j] = t;
-    kc.gtab[16 + j] = kc.cpos[mstart];
-    kc.gcode[j] = 0u;
-    kc.gcode[16 + j] = static_cast<uint32_t>(mstart | h);
+    kc.gval[j] = kc.cpos[mstart];
+    kc.gcode[j] = static_cast<uint32_t>(mstart | h);
+    kc.gtab[16 + j] = inf;
+    kc.gval[16 + j] = 0.0f;
+    kc.gcode[16 + j] = 0u;
   }
   // check the decision at every threshold, its fp32 neighbours and every
   // cell boundary against the counting definition
@@ -174,9 +176,9 @@ bool build_grid(KCodebook& kc, int h, std::string* err) {
     float fl = std::floor(u);
     uint32_t j = fl >= static_cast<float>(nc - 1) ? static_cast<uint32_t>(nc - 1) : static_cast<uint32_t>(fl);
     const float dlt = kc.gtab[j] - u;                            // the kernel's test
-    const uint32_t idx = (j + (std::signbit(dlt) ? 1u : 0u)) & 15u;
-    const int got = static_cast<int>(kc.gcode[16 + idx]) - h;
-    if (got != want || kc.gtab[16 + idx] != kc.cpos[want]) {
+    const uint32_t idx = (j + (std::signbit(dlt) ? 1u : 0u)) & 31u;
+    const int got = static_cast<int>(kc.gcode[idx]) - h;
+    if (got != want || kc.gval[idx] != kc.cpos[want]) {
       *err = "grid: decision table self-check failed";
       return false;
     }

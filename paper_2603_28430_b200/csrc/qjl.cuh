@@ -256,8 +256,8 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
       load_ops<Gm>(mat, sub, P);
     }
     const float ctab = cb.cent[lane & ((1 << BITS) - 1)];
-    const float inv_gscale = 1.0f / cb.gscale;       // a power of two: exact
     const float gtab = cb.gtab[lane];
+    const float gval = cb.gval[lane];
     const uint32_t gcode = cb.gcode[lane];
     const int quad = warp & 3, part = warp >> 2;      // TMEM lane quadrant, column slice
     constexpr int CW = Q::CW;                         // columns per epilogue warp
@@ -326,8 +326,6 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
         const float2 rinv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
         const float2 nrho = f2(-rho.x, -rho.y);
-        // max(rho, eps) / S: undoes the grid's scaling of the rotated row (ROTD, b = 4)
-        const float2 isc = mul2(f2(fmaxf(rho.x, 1e-12f), fmaxf(rho.y, 1e-12f)), bc(inv_gscale));
 
         // ---- stage 1: codes (the iq_quantize rule) and x^ in fp32
         float2 out[EPL];
@@ -338,25 +336,22 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
           const float2 sc = mul2(rinv, bc(cb.gscale));
 #pragma unroll
           for (int b = 0; b < NBL; ++b) {
-            float2 xs[PW], yb[PW], cq[PW];
+            float2 yb[PW], cq[PW];
             float Mb[PW * PW];
             fetch_op<Gm>(P, ops, sub, b, Mb);
-#pragma unroll
-            for (int jv = 0; jv < PW; ++jv) xs[jv] = mul2(v[b * PW + jv], sc);
-            rot_fwd<PW>(Mb, xs, yb);
+            rot_fwd<PW>(Mb, v + b * PW, yb);              // T x (unnormalised)
 #pragma unroll
             for (int jv = 0; jv < PW; ++jv) {
-              const uint32_t ia = grid_index(yb[jv].x, gtab, cb.gclamp);
-              const uint32_t ib = grid_index(yb[jv].y, gtab, cb.gclamp);
+              const uint32_t ia = grid_index(yb[jv].x, sc.x, gtab, cb.gclamp);
+              const uint32_t ib = grid_index(yb[jv].y, sc.y, gtab, cb.gclamp);
               const int e = (b * PW + jv) % EPC, c = (b * PW + jv) / EPC;
               cwa[c] |= grid_code<BITS>(ia, yb[jv].x, gcode) << (e * BITS);
               cwb[c] |= grid_code<BITS>(ib, yb[jv].y, gcode) << (e * BITS);
-              cq[jv] = f2(sign_xor(__shfl_sync(kFull, gtab, (int)ia), yb[jv].x),
-                          sign_xor(__shfl_sync(kFull, gtab, (int)ib), yb[jv].y));
+              cq[jv] = f2(grid_value(ia, yb[jv].x, gval), grid_value(ib, yb[jv].y, gval));
             }
-            if constexpr (Q::ROTD) {                   // r' = T x - rho c, T x = yb max(rho, eps) / S
+            if constexpr (Q::ROTD) {                   // r' = T x - rho c
 #pragma unroll
-              for (int jv = 0; jv < PW; ++jv) out[b * PW + jv] = fma2(cq[jv], nrho, mul2(yb[jv], isc));
+              for (int jv = 0; jv < PW; ++jv) out[b * PW + jv] = fma2(cq[jv], nrho, yb[jv]);
             } else {
               rot_inv<PW>(Mb, cq, out + b * PW);        // T^-1(C[code]); rho applied with r below
             }
