@@ -33,6 +33,8 @@ VARIANTS = {
     "stwb": ["-DIQ_STORE_CS=0"],            # ordinary (write-back) output stores
     "dec16": ["-DIQ_TPL_DEC=16"],           # 16 coordinates per lane in the dequantizer
     "dec4": ["-DIQ_TPL_DEC=4"],             # 4 coordinates per lane in the dequantizer
+    "grid3": ["-DIQ_GRID_MIN_BITS=3"],      # uniform-grid decision also at b = 3
+    "base2": [],                            # second copy of the default (run-order drift)
 }
 
 
