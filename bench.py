@@ -408,6 +408,16 @@ def main():
                                         "bytes_per_launch": b, "keys_per_s": H * nk / (t / 1e3),
                                         "shape": f"{H} heads x {nk} keys, 4 queries per head, stage 1"}
             del qh, sc
+        # context: a plain device-to-device copy of the same bytes (torch's
+        # copy kernel, not on our path) timed the same way on this box
+        if not inplace:
+            t = time_launches(torch, lambda i: ys[i & 1].copy_(xs[i & 1]), max(10, a.steps), 3, stream)
+            b = a.n * 2 * a.d * s
+            gbs = b / (t / 1e3) / 1e9
+            kern["copy_reference"] = {
+                "us": 1e3 * t, "GB/s": gbs, "frac": gbs / peak, "bytes_per_launch": b,
+                "roundtrip_frac_of_copy": kern["roundtrip"]["GB/s"] / gbs,
+                "what": "torch copy_ of x into y (the fused kernel's read + write bytes), library kernel, context only"}
         out["kernels"] = kern
         del codes, norms
 
