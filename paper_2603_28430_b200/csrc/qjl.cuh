@@ -29,6 +29,9 @@ struct QGeo {
 #ifndef IQ_QJL_ROTD
 #define IQ_QJL_ROTD 1
 #endif
+#ifndef IQ_QJL_PASSES
+#define IQ_QJL_PASSES (Q::ROTD ? 3 : 2)   // MMA passes per tile (timing probes override it)
+#endif
 #ifdef IQ_QJL_NWC
   static constexpr int NWC0 = IQ_QJL_NWC;
 #else
@@ -228,7 +231,7 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         const uint32_t td = tmem + b * M;
         // A_hi B_hi + A_lo B_hi (+ A_hi B_lo with S' split in two)
 #pragma unroll
-        for (int part = 0; part < (Q::ROTD ? 3 : 2); ++part) {
+        for (int part = 0; part < IQ_QJL_PASSES; ++part) {
           const uint32_t pa = part == 1 ? al : ah, pb = sb + (part == 2 ? Q::S_BYTES : 0);
 #pragma unroll
           for (int s = 0; s < D / 16; ++s)
