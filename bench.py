@@ -142,8 +142,15 @@ class ClockSampler:
         load = [r for r in rows if t0 - 0.05 <= r[0] <= t1 + 0.15] or rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in load for i, v in enumerate(r[4]) if v.lower() == "active"})
+        watts = []
+        for r in load:
+            try:
+                watts.append(float(r[3]))
+            except ValueError:
+                pass
         return {"sm_mhz": statistics.median(r[1] for r in load), "sm_max_mhz": max(r[2] for r in load),
-                "reasons": reasons, "samples": len(load)}
+                "reasons": reasons, "samples": len(load),
+                "power_w": statistics.median(watts) if watts else None}
 
 
 # ------------------------------------------------------------------ helpers

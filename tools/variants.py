@@ -19,6 +19,8 @@ VARIANTS = {
     "base": [],
     "opsreg": ["-DIQ_OPS_SMEM=0"],          # encoder operators always in registers (8-warp CTAs)
     "nwc12": ["-DIQ_NWC_WIDE=12"],          # 12 compute warps in the wide encoder CTAs
+    "nwc20": ["-DIQ_NWC_WIDE=20"],
+    "nwc24": ["-DIQ_NWC_WIDE=24"],
     "b3fma": ["-DIQ_B3_ALU=0"],             # b = 3 chain as FSET + FFMA2
     "stage64": ["-DIQ_STAGE_KB=64"],        # 64 KB ring stages
     "tchint": ["-DIQ_TC_SPIN=0"],           # suspend-hint waits on tcgen05.commit barriers
