@@ -15,7 +15,9 @@ Timing: W untimed warm-up steps, a short untimed clock-settle loop, then
 EXACTLY K steps bracketed by barrier + cuda.synchronize on both sides, CUDA
 events on the launching stream, max over ranks.  Inputs (256 MiB per buffer
 at the headline setting) exceed the 126 MB L2 and two buffer sets rotate.
-rank 0 prints ONE JSON line.
+The kernel-level entries ("kernels", "sweep") are the median of three
+back-to-back windows of CUDA-event-timed launches.  rank 0 prints ONE JSON
+line.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
@@ -180,18 +182,23 @@ def bytes_per_vector(kind: str, d: int, bits: int, s: int) -> int:
             "quantize_qjl": d * s + code + 4 + d // 8 + 4}[kind]
 
 
-def time_launches(torch, fn, reps: int, warm: int, stream) -> float:
-    """ms per launch: CUDA events on the launching stream, after warm-up."""
+def time_launches(torch, fn, reps: int, warm: int, stream, repeats: int = 3) -> float:
+    """ms per launch: CUDA events on the launching stream, after warm-up;
+    the median of `repeats` back-to-back windows of `reps` launches (one
+    window can catch a transient clock dip)."""
     for i in range(warm):
         fn(i)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(reps):
-        fn(i)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    out = []
+    for _ in range(repeats):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(reps):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / reps)
+    return statistics.median(out)
 
 
 # ------------------------------------------------------------------ reference arm
