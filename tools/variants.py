@@ -40,9 +40,6 @@ VARIANTS = {
     "qjl0mma": ["-DIQ_QJL_PASSES=0"],       # timing probe only: no MMAs issued (wrong sketch)
     "qjl1mma": ["-DIQ_QJL_PASSES=1"],       # timing probe only: one MMA pass (inexact sketch)
     "norotd": ["-DIQ_QJL_ROTD=0"],          # stage 2 residual in the input domain (2 passes)
-    "sat1": ["-DIQ_B3_SAT=1"],              # b = 3 value chain: threshold 1 as FFMA.SAT + FFMA2
-    "sat2": ["-DIQ_B3_SAT=2"],              # thresholds 1-2
-    "sat3": ["-DIQ_B3_SAT=3"],              # all three
 }
 
 
