@@ -29,6 +29,9 @@ struct QGeo {
 #ifndef IQ_QJL_ROTD
 #define IQ_QJL_ROTD 1
 #endif
+#ifndef IQ_QJL_NOWAIT_PROBE
+#define IQ_QJL_NOWAIT_PROBE 0   // timing probe only: compute warps do not wait for the A tile (racy)
+#endif
 #ifndef IQ_QJL_PASSES
 #define IQ_QJL_PASSES (Q::ROTD ? 3 : 2)   // MMA passes per tile (timing probes override it)
 #endif
@@ -416,7 +419,9 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         const float2 sr = mul2(rinv, bc(256.0f));
         // the previous tile's MMAs must have consumed the A tiles (the
         // stage-1 work above overlaps them)
+#if !IQ_QJL_NOWAIT_PROBE
         if (u == 0) mbar_wait(a_free, (j & 1) ^ 1);
+#endif
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           float ta[EPC], tb[EPC];

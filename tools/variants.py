@@ -39,6 +39,7 @@ VARIANTS = {
     "base2": [],                            # second copy of the default (run-order drift)
     "qjl0mma": ["-DIQ_QJL_PASSES=0"],       # timing probe only: no MMAs issued (wrong sketch)
     "qjl1mma": ["-DIQ_QJL_PASSES=1"],       # timing probe only: one MMA pass (inexact sketch)
+    "qjlnowait": ["-DIQ_QJL_NOWAIT_PROBE=1"],   # timing probe only: A tile reuse without the MMA wait (racy)
     "norotd": ["-DIQ_QJL_ROTD=0"],          # stage 2 residual in the input domain (2 passes)
 }
 
