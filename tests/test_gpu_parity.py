@@ -255,3 +255,29 @@ def test_norms_over_many_fresh_launches(d, bits, dt):
         _, _, ne = iq.iq_roundtrip(p, x, emit_codes=True)
         bad += int(((nq - tn).abs() / tn > 1e-5).sum()) + int(((ne - tn).abs() / tn > 1e-5).sum())
     assert bad == 0
+
+
+@pytest.mark.gpu
+def test_quantize_outputs_at_4_byte_alignment():
+    """The ABI promises codes and norms need only 4-byte alignment for
+    iq_quantize / iq_roundtrip (include/isoquant.h): outputs at a 4-byte
+    offset equal the 16-byte-aligned ones, bit for bit."""
+    for d, bits, dt in ((128, 3, np.float16), (64, 4, np.float32), (256, 2, np.float16)):
+        n = 1000
+        X = iqsynth.unit_vectors(n, d, 21, dt)
+        x = torch.from_numpy(X).cuda()
+        p = iq.iq_make_params(d, bits, iq.FULL, SEED, device=0)
+        cb = p.code_bytes
+        c0 = torch.empty((n, cb), dtype=torch.uint8, device="cuda")
+        r0 = torch.empty(n, dtype=torch.float32, device="cuda")
+        iq.iq_quantize(p, x, c0, r0)
+        craw = torch.zeros(n * cb + 16, dtype=torch.uint8, device="cuda")
+        rraw = torch.zeros(n + 4, dtype=torch.float32, device="cuda")
+        c1 = craw[4:4 + n * cb].view(n, cb)
+        r1 = rraw[1:1 + n]
+        iq.iq_quantize(p, x, c1, r1)
+        assert torch.equal(c0, c1) and torch.equal(r0, r1)
+        y1 = torch.empty_like(x)
+        c2, r2 = craw[8:8 + n * cb].view(n, cb), rraw[3:3 + n]
+        iq.iq_roundtrip(p, x, y=y1, codes=c2, norms=r2)
+        assert torch.equal(c0, c2) and torch.equal(r0, r2)
