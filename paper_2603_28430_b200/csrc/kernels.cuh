@@ -173,12 +173,15 @@ struct Geo {
   // rows per stage: >= STAGE_KB of x and a whole number of row pairs per warp
   // (granule: whole row pairs per warp, and 16-byte aligned norm tiles)
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
-  // stage size (measured): 32 KB for the b = 3 encoders and the b = 4 fused
-  // kernel (more rows per warp per mbarrier round trip), else 16 KB
+  // stage size (measured): 64 KB for the 16-bit quantizer at b >= 3, d >= 128
+  // (2-5 % over 32 / 16 KB; worse at fp32 and b = 2), 32 KB for the other
+  // b = 3 encoders and the b = 4 fused kernel (more rows per warp per
+  // mbarrier round trip), else 16 KB
 #ifdef IQ_STAGE_KB
   static constexpr int STAGE_KB = ENC ? IQ_STAGE_KB : 16;
 #else
-  static constexpr int STAGE_KB = (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32 : 16;
+  static constexpr int STAGE_KB = (KIND == 0 && sizeof(T) == 2 && BITS >= 3 && D >= 128) ? 64
+                                  : (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32 : 16;
 #endif
   static constexpr int TV0 = (STAGE_KB * 1024 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;
