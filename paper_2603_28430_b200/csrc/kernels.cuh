@@ -180,8 +180,15 @@ struct Geo {
 #ifdef IQ_STAGE_KB
   static constexpr int STAGE_KB = ENC ? IQ_STAGE_KB : 16;
 #else
+#ifndef IQ_DEC_STAGE_KB
+#define IQ_DEC_STAGE_KB 0
+#endif
+  // decoder tiles: 32 KB of output rows at b <= 3 (1-8 % over 16 KB; d = 64
+  // gains most), 16 KB at b = 4 (32 KB: 4-10 % slower)
+  static constexpr int DEC_KB = IQ_DEC_STAGE_KB ? IQ_DEC_STAGE_KB : (BITS <= 3 ? 32 : 16);
   static constexpr int STAGE_KB = (KIND == 0 && sizeof(T) == 2 && BITS >= 3 && D >= 128) ? 64
-                                  : (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32 : 16;
+                                  : (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32
+                                  : ENC ? 16 : DEC_KB;
 #endif
   static constexpr int TV0 = (STAGE_KB * 1024 / ROWB) / GR * GR;
   static constexpr int TILE_V = TV0 > GR ? TV0 : GR;

@@ -24,6 +24,8 @@ VARIANTS = {
     "b3fma": ["-DIQ_B3_ALU=0"],             # b = 3 chain as FSET + FFMA2
     "stage64": ["-DIQ_STAGE_KB=64"],        # 64 KB ring stages
     "stage16": ["-DIQ_STAGE_KB=16"],        # 16 KB ring stages for every encoder
+    "dec16kb": ["-DIQ_DEC_STAGE_KB=16"],    # decoder tiles of 16 / 32 KB of output rows at every b
+    "dec32kb": ["-DIQ_DEC_STAGE_KB=32"],
     "tchint": ["-DIQ_TC_SPIN=0"],           # suspend-hint waits on tcgen05.commit barriers
     "qjl8": ["-DIQ_QJL_NWC=8"],             # 8 compute warps in the stage-2 kernel
     "attn8": ["-DIQ_ATTN_NWD=8"],           # 8 decoder warps in the attention consumer
