@@ -251,15 +251,17 @@ def lloyd_max_gaussian(bits: int, tol: float = 1e-15, max_iter: int = 200000):
 class Codebook:
     """The shared scalar codebook of one (d, b) configuration [R1][R2].
 
-    ``centroids`` are fp32 values (stored in fp64): round_fp32(c_k / sqrt(d)).
-    ``thresholds`` are fp32 midpoints of adjacent fp32 centroids:
-    round_fp32((C_k + C_{k+1}) / 2) — the decision boundaries of nearest-
-    centroid assignment in the kernel's precision [R14b].
+    ``centroids`` are fp32 values (stored in fp64): round_fp32(c_k / sqrt(d))
+    — the codebook as a device stores it [R14b].
+    ``thresholds`` are the fp64 midpoints (C_k + C_{k+1}) / 2 of adjacent
+    centroids (exact in fp64: both are fp32 values) — the decision boundaries
+    of nearest-centroid assignment, NOT rounded to fp32: the oracle
+    decides in fp64 [R14b].
     """
     bits: int
     d: int
     centroids: np.ndarray    # [L] fp32-representable, dtype float64
-    thresholds: np.ndarray   # [L-1] dtype float32
+    thresholds: np.ndarray   # [L-1] dtype float64, exact midpoints
     levels_unit: np.ndarray  # [L] fp64 N(0,1) Lloyd-Max levels
 
 
@@ -269,27 +271,26 @@ def make_codebook(d: int, bits: int) -> Codebook:
     levels, _ = lloyd_max_gaussian(bits)
     C32 = (levels / math.sqrt(d)).astype(np.float32)
     C = C32.astype(np.float64)
-    T = ((C[:-1] + C[1:]) * 0.5).astype(np.float32)
+    T = (C[:-1] + C[1:]) * 0.5
     return Codebook(bits=bits, d=d, centroids=C, thresholds=T, levels_unit=levels)
 
 
 def quantize_codes(y: np.ndarray, cb: Codebook) -> np.ndarray:
-    """Nearest-centroid code of every coordinate (v^ = Q(v~)).  The
-    paper does not say how a value exactly half-way between two centroids
-    is coded; reading [R3]: the tie goes to the centroid of LARGER MAGNITUDE
-    (away from zero), and y = +-0 codes on the positive side, so the
-    quantizer of a symmetric codebook is odd: Q(-y) = -Q(y) for y != 0.
-    With the sorted thresholds t_k (midpoints of adjacent centroids):
-        y >= 0 : code = #{k : y >= t_k}
-        y <  0 : code = #{k : y >  t_k}
-    Values beyond the extreme thresholds clamp to the end codes [R4].  The
-    decision is taken in fp32, the kernel's precision [R14b]: y is rounded to
-    fp32 and compared with the fp32 thresholds."""
-    y32 = np.asarray(y).astype(np.float32)
-    nonneg = y32 >= 0
-    codes = np.zeros(y32.shape, dtype=np.int64)
+    """Nearest-centroid code of every coordinate (v^ = Q(v~); Alg.1
+    l.6), written as the count over the sorted thresholds t_k (the
+    midpoints of adjacent centroids):
+
+        code = #{k : y >= t_k}
+
+    in fp64 on the fp64 rotated coordinate [R14b].  This is argmin_k
+    |y - C_k| except at an exact midpoint, where the paper is silent
+    (P:182); reading [R3] takes the upper code there, so y = +-0
+    codes on the positive side (-0 >= 0).  Values beyond the extreme
+    thresholds clamp to the end codes [R4] (automatic with counting)."""
+    y = np.asarray(y, dtype=np.float64)
+    codes = np.zeros(y.shape, dtype=np.int64)
     for t in cb.thresholds:
-        codes += np.where(nonneg, y32 >= t, y32 > t)
+        codes += (y >= t)
     return codes
 
 

@@ -61,8 +61,11 @@ def test_codebook_structure():
             assert np.all(np.diff(C) > 0) and np.all(np.diff(T) > 0)
             assert np.array_equal(C.astype(np.float32).astype(np.float64), C)
             assert np.array_equal(T, -T[::-1])
-            mid = ((C[:-1] + C[1:]) / 2).astype(np.float32)
-            assert np.array_equal(T, mid)
+            # exact fp64 midpoints of the fp32 centroids [R14b]: 2T - C_k is
+            # C_{k+1} bit for bit (no rounding anywhere)
+            assert T.dtype == np.float64
+            assert np.array_equal(2.0 * T - C[:-1], C[1:])
+            assert np.array_equal(2.0 * T - C[1:], C[:-1])
             # scaled by 1/sqrt(d): variance-1/d coordinates (P:273 with k=d)
             assert np.allclose(C * math.sqrt(d), cb.levels_unit, rtol=1e-6)
 
@@ -70,7 +73,7 @@ def test_codebook_structure():
 # ------------------------------------------------------------ quantize [R3][R4]
 def _custom_codebook(levels):
     C = np.asarray(levels, dtype=np.float32).astype(np.float64)
-    T = ((C[:-1] + C[1:]) / 2).astype(np.float32)
+    T = (C[:-1] + C[1:]) / 2
     return O.Codebook(bits=int(math.log2(len(C))), d=1, centroids=C, thresholds=T, levels_unit=C)
 
 
@@ -80,44 +83,52 @@ def test_spec_quantizer_examples():
         assert int(O.quantize_codes(np.array([c["v"]]), cb)[0]) == c["code"]
 
 
-def test_ties_away_from_zero_and_signed_zero():
-    """[R3]: a value exactly on a threshold takes the larger-magnitude
-    centroid; +-0 code on the positive side."""
+def test_ties_go_up_and_signed_zero():
+    """[R3]: a value exactly on a threshold takes the upper code, at
+    negative thresholds too; +-0 code on the positive side; the count clamps
+    [R4].  The SPEC's negative-threshold example: levels (-.75,-.25,.25,.75),
+    v = -0.5 (the midpoint of -0.75 and -0.25) codes 1."""
     cb = O.make_codebook(128, 3)
     T = cb.thresholds                                                    # t_0..t_6, t_3 = 0
-    codes = O.quantize_codes(T.astype(np.float64), cb)
-    assert np.array_equal(codes, [0, 1, 2, 4, 5, 6, 7])                 # t_k<0 -> k, t_k>=0 -> k+1
+    codes = O.quantize_codes(T, cb)
+    assert np.array_equal(codes, [1, 2, 3, 4, 5, 6, 7])                 # t_k -> k+1
     assert O.quantize_codes(np.array([0.0, -0.0]), cb).tolist() == [4, 4]   # +-0 -> upper half
     assert O.quantize_codes(np.array([-1e9, 1e9]), cb).tolist() == [0, 7]   # clamp
-    toward0 = np.where(T < 0, np.nextafter(T, np.inf, dtype=np.float32),
-                       np.nextafter(T, -np.inf, dtype=np.float32)).astype(np.float64)
-    assert np.array_equal(O.quantize_codes(toward0, cb), [1, 2, 3, 3, 4, 5, 6])
+    below = np.nextafter(T, -np.inf)                                     # one fp64 ulp below
+    assert np.array_equal(O.quantize_codes(below, cb), [0, 1, 2, 3, 4, 5, 6])
+    spec = _custom_codebook([-0.75, -0.25, 0.25, 0.75])
+    assert O.quantize_codes(np.array([-0.5, 0.5, 0.0]), spec).tolist() == [1, 3, 2]
 
 
-def test_quantizer_is_odd():
-    """Q(-y) = -Q(y) for y != 0, ties included (symmetric codebook [R2])."""
+def test_quantizer_is_odd_off_ties():
+    """Q(-y) = -Q(y) for every y that is not a threshold (symmetric codebook
+    [R2]); at a nonzero threshold the tie rule breaks the symmetry by one
+    level (ties go up on both sides)."""
     rng = np.random.default_rng(11)
     for b in (1, 2, 3, 4):
         cb = O.make_codebook(256, b)
-        y = np.concatenate([(rng.standard_normal(5000) * 0.08).astype(np.float32).astype(np.float64),
-                            cb.thresholds.astype(np.float64)])
-        y = y[y != 0]
+        y = (rng.standard_normal(5000) * 0.08)
+        y = y[np.min(np.abs(np.abs(y)[:, None] - cb.thresholds[None, :]), axis=1) > 0]
         qp = O.dequantize_codes(O.quantize_codes(y, cb), cb)
         qn = O.dequantize_codes(O.quantize_codes(-y, cb), cb)
         assert np.array_equal(qn, -qp)
+        t = cb.thresholds[cb.thresholds > 0]
+        if t.size:
+            up, dn = O.quantize_codes(t, cb), O.quantize_codes(-t, cb)
+            assert np.array_equal(up + dn, np.full(t.shape, (1 << b)))   # symmetric would give L-1
 
 
 def test_nearest_centroid_brute_force():
     """code == argmin_k |y - C_k| (ties to the larger k), by brute force over
-    all L centroids, on random fp32 values away from fp32 rounding of the
-    midpoints (exact midpoints are covered by the tie test)."""
+    all L centroids, on random fp64 values plus values 1e-15 on either side
+    of every midpoint (exact midpoints are covered by the tie test; the
+    brute-force distances resolve ~1e-17 here)."""
     rng = np.random.default_rng(7)
     for b in (1, 2, 3, 4):
         cb = O.make_codebook(128, b)
-        y = (rng.standard_normal(20000) * 0.12).astype(np.float32).astype(np.float64)
         mids = (cb.centroids[:-1] + cb.centroids[1:]) / 2
-        far = np.min(np.abs(y[:, None] - mids[None, :]), axis=1) > 1e-7
-        y = y[far]
+        y = np.concatenate([rng.standard_normal(20000) * 0.12,
+                            mids + 1e-15, mids - 1e-15])
         dist = np.abs(y[:, None] - cb.centroids[None, :])
         L = len(cb.centroids)
         brute = L - 1 - np.argmin(dist[:, ::-1], axis=1)     # ties -> larger k
