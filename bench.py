@@ -48,6 +48,25 @@ FALLBACK_HBM_GBS = 6650.0
 VARIANT_NAMES = {0: "full", 1: "fast", 2: "planar2d"}
 
 
+# BASELINE.json configs as bench presets.  The strong-scaling ones keep the
+# global batch (and so its MSE) identical at every GPU count: cfg3's KV cache
+# is split by layer (32/G layers per rank), cfg5's 2^26 rows by contiguous
+# row ranges.
+PRESETS = {
+    "headline": dict(variant="full", d=128, bits=3, dtype="f16", n=1 << 20, scaling="weak", config=2,
+                     what="configs[1] headline, Full d=128 b=3 fp16, 2^20 vectors per GPU (weak)"),
+    "cfg1": dict(variant="full", d=128, bits=3, dtype="f32", n=4096, scaling="weak", config=1,
+                 what="configs[0] Full d=128 b=3 fp32, 4096 vectors (L2-resident latency case)"),
+    "cfg3": dict(variant="fast", d=128, bits=4, dtype="f16", n=32 * 8 * 32768, scaling="strong", config=3,
+                 what="configs[2] KV cache [32 layers, 8 heads, 32768 tokens] Fast d=128 b=4 fp16, "
+                      "32/G layers per GPU (strong)"),
+    "cfg4": dict(variant="planar2d", d=256, bits=2, dtype="f16", n=1 << 24, scaling="strong", config=4,
+                 what="configs[3] 2D d=256 b=2 fp16, 16M vectors (strong)"),
+    "cfg5": dict(variant="full", d=512, bits=2, dtype="f16", n=1 << 26, scaling="strong", config=5,
+                 what="configs[4] Full d=512 b=2 fp16, 64M vectors across the GPUs (strong)"),
+}
+
+
 def parse_args():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -58,7 +77,11 @@ def parse_args():
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--bits", type=int, default=3)
     ap.add_argument("--dtype", default="f16", choices=["f16", "f32"])
-    ap.add_argument("--n", type=int, default=1 << 20, help="vectors per GPU")
+    ap.add_argument("--n", type=int, default=1 << 20,
+                    help="vectors per GPU (weak scaling) or in the global batch (strong scaling)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--preset", choices=sorted(PRESETS), default=None,
+                    help="a BASELINE.json config: " + "; ".join(f"{k}: {v['what']}" for k, v in PRESETS.items()))
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -67,11 +90,19 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: headline loop only, no extras")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.config = 2
+    if a.preset:
+        for k, v in PRESETS[a.preset].items():
+            if k != "what":
+                setattr(a, k, v)
+    return a
 
 
 def config_name(a):
     """Which BASELINE.json configs[] entry the arguments describe."""
+    if a.preset:
+        return PRESETS[a.preset]["what"]
     key = (a.variant, a.d, a.bits, a.dtype)
     if key == ("fast", 128, 4, "f16") and a.n == 32 * 8 * 32768:
         return "configs[2] KV-cache shaped (32 layers x 8 KV heads x 32k tokens)"
@@ -85,15 +116,29 @@ def config_name(a):
 
 
 def workload_config(a, world):
+    n_global = a.n * world if a.scaling == "weak" else a.n
+    per = "per GPU" if a.scaling == "weak" else "in the global batch"
     return {
         "workload": (f"{config_name(a)}: IsoQuant-{a.variant.capitalize()} d={a.d} b={a.bits} "
-                     f"{'fp16' if a.dtype == 'f16' else 'fp32'}, {a.n} synthetic unit vectors per GPU"),
-        "variant": a.variant, "d": a.d, "bits": a.bits, "io_dtype": a.dtype, "n_per_gpu": a.n,
-        "global_vectors": a.n * world, "parallelism": f"dp{world} (vectors sharded by batch)",
-        "step": "one fused roundtrip launch (iq_roundtrip) over the batch",
+                     f"{'fp16' if a.dtype == 'f16' else 'fp32'}, {a.n} synthetic unit vectors {per}"),
+        "variant": a.variant, "d": a.d, "bits": a.bits, "io_dtype": a.dtype,
+        "n_per_gpu": a.n if a.scaling == "weak" else None, "global_vectors": n_global,
+        "parallelism": f"dp{world} (vectors sharded by contiguous row ranges, no collective on the hot path)",
+        "step": "one fused roundtrip launch (iq_roundtrip, no code emission) over the rank's rows",
+        "data_seeding": "chunk-seeded global batch (iqsynth.dist.rank_buffers): a rank draws exactly its rows",
         "l2": "inputs larger than L2 (>=256 MiB per buffer vs 126 MB) and 2 rotating buffer sets "
-              "(1 set, or in place, when they do not fit HBM)",
+              "(1 set, or in place, when they do not fit HBM)" if rank_rows(a, world) * a.d * dsize(a) >= (256 << 20)
+              else "L2-resident (a latency configuration, not a bandwidth one)",
     }
+
+
+def dsize(a) -> int:
+    return 2 if a.dtype == "f16" else 4
+
+
+def rank_rows(a, world) -> int:
+    """Rows of the largest rank (the one the max-over-ranks time is set by)."""
+    return a.n if a.scaling == "weak" else -(-a.n // world)
 
 
 # ------------------------------------------------------------------ clocks
@@ -201,64 +246,152 @@ def time_launches(torch, fn, reps: int, warm: int, stream, repeats: int = 3) -> 
     return statistics.median(out)
 
 
+# ------------------------------------------------------------------ CPU oracle
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _oracle_work(args):
+    """One worker: the oracle (as it stands) on `reps` batches of `batch`
+    rows of the workload; single-threaded NumPy.  Returns (rows, seconds)."""
+    variant, d, bits, dtype, batch, reps, seed = args
+    from threadpoolctl import threadpool_limits
+    import numpy as np
+    import iqsynth
+    from oracle import iq_oracle as O
+    with threadpool_limits(1):
+        po = O.make_params(d, bits, {"full": O.FULL, "fast": O.FAST, "planar2d": O.PLANAR2D}[variant],
+                           iqsynth.PARAMS_SEED)
+        X = iqsynth.unit_vectors(batch, d, seed, np.float16 if dtype == "f16" else np.float32)
+        O.roundtrip(X[:64], po)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            O.roundtrip(X, po)
+        return batch * reps, time.perf_counter() - t0
+
+
+class OraclePool:
+    """The oracle on every host core (one single-threaded process per core,
+    spawn start), plus the single-process figure, on bounded samples."""
+
+    def __init__(self, a):
+        import multiprocessing as mp
+        self.a = a
+        self.cores = host_cores()
+        self.pool = mp.get_context("spawn").Pool(self.cores)
+        self.batch = 8192 if a.d <= 256 else 4096
+
+    def run(self, reps: int):
+        """Every core processes `reps` batches; returns (vectors, wall s)."""
+        a = self.a
+        jobs = [(a.variant, a.d, a.bits, a.dtype, self.batch, reps, iqsynth_seed(a, i)) for i in range(self.cores)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_work, jobs)
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def iqsynth_seed(a, i: int) -> int:
+    return 1000 * a.config + 500 + i
+
+
+def cpu_baseline(a, seconds: float):
+    """The oracle as it stands, on the host cores, on a bounded sample: one
+    process alone, then one process per core (all cores busy)."""
+    n1, t1 = _oracle_work((a.variant, a.d, a.bits, a.dtype, 8192 if a.d <= 256 else 4096, 1, 1000 * a.config + 499))
+    reps = max(1, int(0.25 * seconds / max(t1, 1e-3)))
+    n1, t1 = _oracle_work((a.variant, a.d, a.bits, a.dtype, 8192 if a.d <= 256 else 4096, reps,
+                           1000 * a.config + 499))
+    pool = OraclePool(a)
+    try:
+        pool.run(1)                                          # workers up, imports done
+        reps_all = max(1, int(0.6 * seconds / max(t1 / reps, 1e-3)))
+        nall, tall = pool.run(reps_all)
+    finally:
+        pool.close()
+    return {"value": nall / tall, "unit": "vectors/s", "cores": pool.cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{nall} vectors ({reps_all} batches of {pool.batch} per core on {pool.cores} cores, "
+                      f"one single-threaded fp64 NumPy process per core, {tall:.1f} s wall) of the same workload",
+            "single_core": {"value": n1 / t1, "unit": "vectors/s", "cores": 1,
+                            "sample": f"{n1} vectors, {t1:.1f} s, one process"}}
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(a):
+    """The CPU oracle as the reference arm, on all host cores, rank 0 only;
+    each step = every core coding one bounded batch of the workload."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
     if rank != 0:
         return
-    import numpy as np
-    import iqsynth
-    from oracle import iq_oracle as O
-    vid = {"full": O.FULL, "fast": O.FAST, "planar2d": O.PLANAR2D}[a.variant]
-    po = O.make_params(a.d, a.bits, vid, iqsynth.PARAMS_SEED)
-    npdt = np.float16 if a.dtype == "f16" else np.float32
-    batch = 8192
-    X = iqsynth.unit_vectors(batch, a.d, iqsynth.data_seed(2), npdt)
-    for _ in range(a.warmup):
-        O.roundtrip(X, po)
-    t0 = time.perf_counter()
-    for _ in range(a.steps):
-        O.roundtrip(X, po)
-    t = time.perf_counter() - t0
-    v = batch * a.steps / t
+    pool = OraclePool(a)
+    try:
+        for _ in range(a.warmup):
+            pool.run(1)
+        done, t = 0, 0.0
+        for _ in range(a.steps):
+            n, dt = pool.run(1)
+            done += n
+            t += dt
+    finally:
+        pool.close()
+    v = done / t
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "vectors/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(a, world),
-        "cpu_baseline": {"value": v, "unit": "vectors/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{batch} vectors per step (the paper's batch, P:371) of the same workload, "
-                                   f"fp64 NumPy oracle, single process"},
+        "cpu_baseline": {"value": v, "unit": "vectors/s", "cores": pool.cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"{pool.batch} vectors per core per step ({pool.cores} cores, one single-threaded "
+                                   f"fp64 NumPy oracle process per core) of the same workload"},
         "e2e": {"value": v, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(a, seconds: float):
-    """The oracle as it stands, on the host cores, on a bounded sample."""
-    import numpy as np
-    import iqsynth
-    from oracle import iq_oracle as O
-    vid = {"full": O.FULL, "fast": O.FAST, "planar2d": O.PLANAR2D}[a.variant]
-    po = O.make_params(a.d, a.bits, vid, iqsynth.PARAMS_SEED)
-    npdt = np.float16 if a.dtype == "f16" else np.float32
-    batch = 8192
-    X = iqsynth.unit_vectors(batch, a.d, iqsynth.data_seed(2), npdt)
-    O.roundtrip(X[:64], po)
-    done, t0 = 0, time.perf_counter()
-    while True:
-        O.roundtrip(X, po)
-        done += batch
-        t = time.perf_counter() - t0
-        if t >= seconds or done >= 64 * batch:
-            break
-    return {"value": done / t, "unit": "vectors/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} vectors ({done // batch} batches of {batch}) of the same workload, "
-                      f"{t:.1f} s, fp64 NumPy oracle, single process"}
-
-
 # ------------------------------------------------------------------ our arm
+def sustained_time(torch, fn, steps: int, stream, settle_s: float, barrier=lambda: None) -> float:
+    """ms for `steps` back-to-back launches after an untimed clock-settle loop
+    of `settle_s` seconds under the same load (CUDA events on the launching
+    stream, synchronize + barrier on both sides)."""
+    t0 = time.time()
+    i = 0
+    while time.time() - t0 < settle_s:
+        fn(i)
+        i += 1
+        if i % 64 == 0:
+            torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        fn(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    return e0.elapsed_time(e1)
+
+
 def main():
     a = parse_args()
     if a.impl == "reference":
@@ -266,7 +399,6 @@ def main():
 
     import torch
     import torch.distributed as dist
-    import numpy as np
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -275,18 +407,22 @@ def main():
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl = None
     if world > 1:
+        # NCCL's init lines (communicator size, transports, NVLS) on stderr, so
+        # the communicator is verifiable without mixing into the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
+        one = torch.ones(1, device=dev)
+        dist.all_reduce(one)                                   # communicator up: counts the ranks
+        nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "allreduce_of_ones": int(one.item()), "version": ".".join(map(str, torch.cuda.nccl.version()))}
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local])
-
-    def allreduce(vals, op):
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=op)
-        return t.tolist()
 
     from __graft_entry__ import load_builder
     _build = load_builder()
@@ -299,18 +435,19 @@ def main():
 
     vid = iq.VARIANTS[a.variant]
     tdt = torch.float16 if a.dtype == "f16" else torch.float32
-    s = 2 if a.dtype == "f16" else 4
+    s = dsize(a)
     p = iq.iq_make_params(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=local)
     stream = torch.cuda.current_stream()
-    # each rank's shard: its own chunk seeds (weak scaling, no data movement)
-    # two rotating buffer sets while they fit; one set (y separate) or in place
-    # (y = x, allowed by the ABI) for the largest configs (cfg5: 64 GiB per buffer)
-    buf = a.n * a.d * s
+    # this rank's rows of the chunk-seeded global batch (weak: its own 2^20
+    # rows; strong: its contiguous share, e.g. 32/G layers of the KV cache);
+    # two rotating buffer sets while they fit, else one set (y separate) or
+    # in place (y = x, allowed by the ABI) for the largest configs
+    row0, rows, n_global = D.plan_rows(a.scaling, a.n, world, rank)
+    buf = rows * a.d * s
     free_b = torch.cuda.mem_get_info(dev)[0]
     nsets = 2 if 4 * buf <= 0.8 * free_b else 1
     inplace = nsets == 1 and 2 * buf > 0.8 * free_b
-    xs = [iqsynth.device_unit_vectors(a.n, a.d, D.shard_seed(2, rank, j), tdt, dev)
-          for j in range(nsets)]
+    xs, _, _ = D.rank_buffers(a.config, a.n, a.d, tdt, dev, a.scaling, world, rank, buffers=nsets)
     ys = xs if inplace else [torch.empty_like(x) for x in xs]
     if nsets == 1:
         xs, ys = xs * 2, ys * 2
@@ -326,53 +463,49 @@ def main():
         sampler.start()
         time.sleep(0.3)
     t_load0 = time.time()
-    i = 0
-    settle = float(os.environ.get("IQ_SETTLE_S", "0.4"))
-    while not a.profile and time.time() - t_load0 < settle:   # untimed clock settle under load
-        step(i)
-        i += 1
-        if i % 64 == 0:
-            torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(a.steps):
-        step(i)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    settle = 0.0 if a.profile else float(os.environ.get("IQ_SETTLE_S", "0.4"))
+    ms = sustained_time(torch, step, a.steps, stream, settle, barrier)
     t_end = time.time()
-    ms = e0.elapsed_time(e1)
     clocks = sampler.stop(t_load0, t_end) if sampler else None
-    # reconstruction sums over every rank's full batch (after timing), then one
-    # combine: MAX of the step time, SUM of the statistics (NCCL at N > 1)
+    # per-rank step times, then one combine: MAX of the step time, SUM of the
+    # reconstruction statistics over every rank's rows (NCCL at N > 1)
+    per_rank = [ms / a.steps]
+    if world > 1:
+        g = [None] * world
+        dist.all_gather_object(g, ms / a.steps)
+        per_rank = g
     sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    for j in range(2):
-        iq.iq_error_sums(p, xs[j], ys[j], sums)
-    ms_max, se_tot, _, cnt_tot = D.combine_stats(ms, *sums.tolist(), 2.0 * a.n * a.d, device=dev)
+    iq.iq_error_sums(p, xs[0], ys[0], sums)
+    ms_max, se_tot, _, cnt_tot = D.combine_stats(ms, *sums.tolist(), float(rows * a.d), device=dev)
     mse = None if inplace else se_tot / cnt_tot
 
     ms_step = ms_max / a.steps
-    value = world * a.n / (ms_step / 1e3)
+    value = n_global / (ms_step / 1e3)
     peak, peak_src = read_peak()
-    bpl = a.n * bytes_per_vector("roundtrip", a.d, a.bits, s)
+    bpl = rows * bytes_per_vector("roundtrip", a.d, a.bits, s)
     achieved = bpl / (ms / a.steps / 1e3) / 1e9
-    key = f"roundtrip_{a.variant}_d{a.d}_b{a.bits}_{a.dtype}_n{a.n}"
+    key = f"roundtrip_{a.variant}_d{a.d}_b{a.bits}_{a.dtype}_n{rows}"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": read_traffic(key),
-                "kernel": f"k_encode<{a.dtype},{a.d},{a.bits},{a.variant},roundtrip>",
-                "algorithmic_bytes_per_launch": bpl, "peak_source": peak_src}
-
+                "traffic_source": "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                  "ncu --set full capture of this kernel at this size, per launch)",
+                "kernel": f"k_encode<{a.dtype},{a.d},{a.bits},{a.variant},MODE 1 (fused, no codes)>",
+                "algorithmic_bytes_per_launch": bpl, "peak_source": peak_src,
+                "timing": "sustained: 0.4 s untimed settle under load, then the K timed steps (CUDA events)"}
 
     out = {
         "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(a, world),
-        "hbm_gbs": world * bpl / (ms_step / 1e3) / 1e9,
+        "hbm_gbs": n_global * bytes_per_vector("roundtrip", a.d, a.bits, s) / (ms_step / 1e3) / 1e9,
         "roofline": roofline, "gpu_launches": a.steps, "clocks": clocks,
-        "mse": {"value": mse, "closed_form": None, "unit": "per coordinate"},
+        "per_rank_ms_per_step": per_rank, "rows_per_rank": [D.plan_rows(a.scaling, a.n, world, r)[1]
+                                                            for r in range(world)],
+        "mse": {"value": mse, "closed_form": None, "unit": "per coordinate",
+                "over": "buffer 0 of every rank's rows (the global batch)"},
     }
+    if nccl:
+        out["nccl"] = nccl
     if not a.profile:
         try:
             from oracle import iq_oracle as O  # closed form only (no oracle on the path)
@@ -380,60 +513,9 @@ def main():
         except Exception:
             pass
 
-    # split kernels + fused-with-codes on the headline config (rank-local)
+    # split kernels + fused-with-codes on this config (rank-local)
     if not (a.profile or a.no_kernels):
-        cb = p.code_bytes
-        codes = torch.empty((a.n, cb), dtype=torch.uint8, device=dev)
-        norms = torch.empty(a.n, dtype=torch.float32, device=dev)
-        kern = {}
-        for name, fn in [
-            ("quantize", lambda i: iq.iq_quantize(p, xs[i & 1], codes, norms, stream=stream)),
-            ("dequantize", lambda i: iq.iq_dequantize(p, codes, norms, y=ys[i & 1], stream=stream)),
-            ("roundtrip_emit", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], codes=codes,
-                                                         norms=norms, stream=stream)),
-            ("roundtrip", step),
-        ]:
-            t = time_launches(torch, fn, max(10, a.steps), 3, stream)
-            b = a.n * bytes_per_vector(name, a.d, a.bits, s)
-            kern[name] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
-                          "bytes_per_launch": b, "vectors_per_s": a.n / (t / 1e3)}
-        if a.d in (64, 128):   # stage-2 residual sketch (tcgen05), NEXT row 1
-            pq = iq.iq_make_params_qjl(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=local)
-            qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device=dev)
-            rn = torch.empty(a.n, dtype=torch.float32, device=dev)
-            t = time_launches(torch, lambda i: iq.iq_quantize_qjl(pq, xs[i & 1], codes, norms, qj, rn,
-                                                                  stream=stream), max(10, a.steps), 3, stream)
-            b = a.n * bytes_per_vector("quantize_qjl", a.d, a.bits, s)
-            kern["quantize_qjl"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
-                                    "bytes_per_launch": b, "vectors_per_s": a.n / (t / 1e3),
-                                    "tensor_tflops": a.n * 4 * a.d * a.d / (t / 1e3) / 1e12}
-            del qj, rn
-        if a.d in (64, 128):   # fused KV-cache decode consumer (NEXT row 2), on this batch as keys
-            H = 32                                  # heads of n/32 keys each, 4 queries per head (GQA)
-            nk = a.n // H
-            qh = torch.randn((H, 4, a.d), dtype=tdt, device=dev)
-            sc = torch.empty((H, 4, nk), dtype=torch.float32, device=dev)
-            c3, n3 = codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk)
-            iq.iq_quantize(p, xs[0][:H * nk], codes[:H * nk], norms[:H * nk], stream=stream)
-            t = time_launches(torch, lambda i: iq.iq_attention_scores(p, c3, n3, qh, scores=sc, stream=stream),
-                              max(10, a.steps), 3, stream)
-            b = H * nk * (p.code_bytes + 4 + 4 * 4)
-            kern["attention_scores"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
-                                        "bytes_per_launch": b, "keys_per_s": H * nk / (t / 1e3),
-                                        "shape": f"{H} heads x {nk} keys, 4 queries per head, stage 1"}
-            del qh, sc
-        # context: a plain device-to-device copy of the same bytes (torch's
-        # copy kernel, not on our path) timed the same way on this box
-        if not inplace:
-            t = time_launches(torch, lambda i: ys[i & 1].copy_(xs[i & 1]), max(10, a.steps), 3, stream)
-            b = a.n * 2 * a.d * s
-            gbs = b / (t / 1e3) / 1e9
-            kern["copy_reference"] = {
-                "us": 1e3 * t, "GB/s": gbs, "frac": gbs / peak, "bytes_per_launch": b,
-                "roundtrip_frac_of_copy": kern["roundtrip"]["GB/s"] / gbs,
-                "what": "torch copy_ of x into y (the fused kernel's read + write bytes), library kernel, context only"}
-        out["kernels"] = kern
-        del codes, norms
+        out["kernels"] = kernel_entries(torch, iq, iqsynth, a, p, xs, ys, rows, vid, dev, stream, peak, inplace)
 
     # end to end through the public host-buffer API (H2D + kernel + D2H timed)
     if not (a.profile or a.no_e2e):
@@ -447,15 +529,19 @@ def main():
             pl.roundtrip(xh, yh)
         t = time.perf_counter() - t0
         barrier()
-        t = allreduce([t], dist.ReduceOp.MAX if world > 1 else None)[0]
-        out["e2e"] = {"value": world * a.n * a.e2e_steps / t, "unit": "vectors/s",
-                      "h2d_bytes_per_step": a.n * a.d * s, "d2h_bytes_per_step": a.n * a.d * s,
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        out["e2e"] = {"value": n_global * a.e2e_steps / t, "unit": "vectors/s",
+                      "h2d_bytes_per_step": rows * a.d * s, "d2h_bytes_per_step": rows * a.d * s,
                       "timing": "host wall clock around the synchronous iq_host_roundtrip call, max over ranks",
                       "api": "iq_host_roundtrip (pinned host buffers, 2^17-vector chunks, 3 streams)"}
         pl.close()
         del xh, yh
 
-    # the 36-setting grid (18 paper settings x Full/Fast), rank 0 at N=1
+    # the 36-setting grid (18 paper settings x Full/Fast), rank 0 at N=1,
+    # each setting timed like the headline (settle, then rotating buffers)
     if rank == 0 and world == 1 and not (a.profile or a.no_sweep):
         del xs, ys
         torch.cuda.empty_cache()
@@ -470,27 +556,94 @@ def main():
         dist.destroy_process_group()
 
 
-def sweep(torch, iq, iqsynth, dev, stream, peak):
+def kernel_entries(torch, iq, iqsynth, a, p, xs, ys, n, vid, dev, stream, peak, inplace):
+    """Every kernel of the path on this config, kernel-level (burst) timing."""
+    s = dsize(a)
+    cb = p.code_bytes
+    codes = torch.empty((n, cb), dtype=torch.uint8, device=dev)
+    norms = torch.empty(n, dtype=torch.float32, device=dev)
+    kern = {}
+    for name, fn in [
+        ("quantize", lambda i: iq.iq_quantize(p, xs[i & 1], codes, norms, stream=stream)),
+        ("dequantize", lambda i: iq.iq_dequantize(p, codes, norms, y=ys[i & 1], stream=stream)),
+        ("roundtrip_emit", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], codes=codes,
+                                                     norms=norms, stream=stream)),
+        ("roundtrip", lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], stream=stream)),
+    ]:
+        t = time_launches(torch, fn, max(10, a.steps), 3, stream)
+        b = n * bytes_per_vector(name, a.d, a.bits, s)
+        kern[name] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                      "bytes_per_launch": b, "vectors_per_s": n / (t / 1e3)}
+    if a.d in (64, 128):   # stage-2 residual sketch (tcgen05), NEXT row 1
+        pq = iq.iq_make_params_qjl(a.d, a.bits, vid, iqsynth.PARAMS_SEED, device=dev.index)
+        qj = torch.empty((n, a.d // 8), dtype=torch.uint8, device=dev)
+        rn = torch.empty(n, dtype=torch.float32, device=dev)
+        t = time_launches(torch, lambda i: iq.iq_quantize_qjl(pq, xs[i & 1], codes, norms, qj, rn,
+                                                              stream=stream), max(10, a.steps), 3, stream)
+        b = n * bytes_per_vector("quantize_qjl", a.d, a.bits, s)
+        kern["quantize_qjl"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                                "bytes_per_launch": b, "vectors_per_s": n / (t / 1e3),
+                                "tensor_tflops": n * 4 * a.d * a.d / (t / 1e3) / 1e12}
+        del qj, rn
+    if a.d in (64, 128) and n >= 32 * 1024:   # fused KV-cache decode consumer (NEXT row 2), the batch as keys
+        H = 32                                  # heads of n/32 keys each, 4 queries per head (GQA)
+        nk = n // H
+        qh = torch.randn((H, 4, a.d), dtype=xs[0].dtype, device=dev)
+        sc = torch.empty((H, 4, nk), dtype=torch.float32, device=dev)
+        c3, n3 = codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk)
+        iq.iq_quantize(p, xs[0][:H * nk], codes[:H * nk], norms[:H * nk], stream=stream)
+        t = time_launches(torch, lambda i: iq.iq_attention_scores(p, c3, n3, qh, scores=sc, stream=stream),
+                          max(10, a.steps), 3, stream)
+        b = H * nk * (p.code_bytes + 4 + 4 * 4)
+        kern["attention_scores"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                                    "bytes_per_launch": b, "keys_per_s": H * nk / (t / 1e3),
+                                    "shape": f"{H} heads x {nk} keys, 4 queries per head, stage 1"}
+        del qh, sc
+    # context: a plain device-to-device copy of the same bytes (torch's copy
+    # kernel, not on our path) timed the same way on this box
+    if not inplace:
+        t = time_launches(torch, lambda i: ys[i & 1].copy_(xs[i & 1]), max(10, a.steps), 3, stream)
+        b = n * 2 * a.d * s
+        gbs = b / (t / 1e3) / 1e9
+        kern["copy_reference"] = {
+            "us": 1e3 * t, "GB/s": gbs, "frac": gbs / peak, "bytes_per_launch": b,
+            "roundtrip_frac_of_copy": kern["roundtrip"]["GB/s"] / gbs,
+            "what": "torch copy_ of x into y (the fused kernel's read + write bytes), library kernel, context only"}
+    return kern
+
+
+def sweep(torch, iq, iqsynth, dev, stream, peak, steps: int = 20, settle_s: float = 0.3):
+    """The 36 settings of configs[1] (d x bits x dtype x {Full, Fast}, 2^20
+    rows), each timed like the headline: two rotating buffer sets larger than
+    L2, an untimed settle loop under load, then `steps` back-to-back launches
+    (CUDA events).  Fractions against the measured HBM peak."""
+    from iqsynth import dist as D
     n = 1 << 20
     rows = []
     for d in (128, 256, 512):
-        base = iqsynth.device_unit_vectors(n, d, iqsynth.data_seed(2, d), torch.float32, dev)
+        base, _, _ = D.rank_buffers(2, n, d, torch.float32, dev, buffers=2)
         for dts, tdt, s in (("f16", torch.float16, 2), ("f32", torch.float32, 4)):
-            x = base.to(tdt) if tdt != torch.float32 else base
-            y = torch.empty_like(x)
+            xs = [b.to(tdt) if tdt != torch.float32 else b for b in base]
+            ys = [torch.empty_like(x) for x in xs]
             for bits in (2, 3, 4):
                 for vname, vid in (("full", 0), ("fast", 1)):
                     p = iq.iq_make_params(d, bits, vid, iqsynth.PARAMS_SEED, device=dev.index)
-                    t = time_launches(torch, lambda i: iq.iq_roundtrip(p, x, y=y, stream=stream), 20, 3, stream)
+                    fn = lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], stream=stream)
+                    for i in range(3):
+                        fn(i)
+                    t = sustained_time(torch, fn, steps, stream, settle_s) / steps
                     b = n * 2 * d * s
                     gbs = b / (t / 1e3) / 1e9
                     rows.append({"variant": vname, "dtype": dts, "d": d, "bits": bits, "us": 1e3 * t,
                                  "GB/s": gbs, "frac": gbs / peak, "vectors_per_s": n / (t / 1e3)})
-            del x, y
+            del xs, ys
         del base
         torch.cuda.empty_cache()
+    fp16 = [r["frac"] for r in rows if r["dtype"] == "f16"]
     return {"n": n, "kernel": "iq_roundtrip (fused, no code emission)", "rows": rows,
-            "min_frac": min(r["frac"] for r in rows)}
+            "timing": f"sustained: {settle_s} s untimed settle, then {steps} timed launches over 2 rotating "
+                      "buffer sets (CUDA events), per setting",
+            "min_frac": min(r["frac"] for r in rows), "min_frac_fp16": min(fp16)}
 
 
 if __name__ == "__main__":

@@ -11,15 +11,18 @@ distribution.  Recipe (DESIGN.md "Input recipe"):
 * outlier channels (tests only): rows g * s with s_j = 4 for j = 0 mod 4 and
   1 otherwise, then normalised — unequal per-coordinate energy, the case the
   paper's decorrelation argument is about.
-* seeds: data seed = 1000 * config + chunk; chunks of 2^20 rows so that any
-  rank can regenerate any chunk (identical global batch at any GPU count).
+* seeds: a global batch is cut into chunks of 2^16 rows; chunk c of the batch
+  with base seed s is drawn from its own seed chunk_seed(s, c) (a SeedSequence
+  hash of the pair, so no two (s, c) share a stream), and any rank can
+  regenerate any chunk: the global batch is identical at every GPU count
+  (``device_unit_vectors(..., row0=...)`` draws global rows [row0, row0+n)).
 """
 from __future__ import annotations
 
 import numpy as np
 
 PARAMS_SEED = 20260331          # parameter seed used by bench and tests
-CHUNK_ROWS = 1 << 20
+CHUNK_ROWS = 1 << 16
 
 
 def data_seed(config: int, chunk: int = 0) -> int:
@@ -60,17 +63,33 @@ def sample_rows(n: int, k: int, seed: int) -> np.ndarray:
     return np.sort(rng.choice(n, size=k, replace=False))
 
 
-def device_unit_vectors(n: int, d: int, seed: int, torch_dtype, device, chunk_rows: int = CHUNK_ROWS):
-    """Device-resident isotropic unit vectors for the large configs, generated
-    chunk by chunk with torch's generator (seed = seed + chunk index);
-    normalised in fp32 and cast.  Returns a contiguous [n, d] tensor."""
+def chunk_seed(seed: int, chunk: int) -> int:
+    """64-bit seed of chunk ``chunk`` of the batch with base seed ``seed``."""
+    st = np.random.SeedSequence([int(seed), int(chunk)]).generate_state(2, np.uint32)
+    return int(st[0]) | (int(st[1]) << 32)
+
+
+def device_unit_vectors(n: int, d: int, seed: int, torch_dtype, device, chunk_rows: int = CHUNK_ROWS,
+                        row0: int = 0):
+    """Device-resident isotropic unit vectors for the large configs: global
+    rows [row0, row0 + n) of the batch with base seed ``seed``.  Chunk c
+    (global rows [c*chunk_rows, (c+1)*chunk_rows)) is drawn whole with torch's
+    generator seeded chunk_seed(seed, c), normalised in fp32 and cast, so a
+    shard of the batch equals the same rows of the whole batch.  Returns a
+    contiguous [n, d] tensor."""
     import torch
     out = torch.empty((n, d), dtype=torch_dtype, device=device)
     gen = torch.Generator(device=device)
-    for c0 in range(0, n, chunk_rows):
-        c1 = min(n, c0 + chunk_rows)
-        gen.manual_seed(seed + c0 // chunk_rows)
-        g = torch.randn((c1 - c0, d), generator=gen, device=device, dtype=torch.float32)
+    r = row0
+    while r < row0 + n:
+        c = r // chunk_rows
+        lo, hi = c * chunk_rows, (c + 1) * chunk_rows
+        take_hi = min(hi, row0 + n)
+        gen.manual_seed(chunk_seed(seed, c))
+        # always the whole chunk (the generator's output for a shorter draw
+        # is not a prefix of the longer one), then the rows wanted
+        g = torch.randn((chunk_rows, d), generator=gen, device=device, dtype=torch.float32)[r - lo:take_hi - lo]
         g = g / g.norm(dim=1, keepdim=True).clamp_min(1e-30)
-        out[c0:c1].copy_(g.to(torch_dtype))
+        out[r - row0:take_hi - row0].copy_(g.to(torch_dtype))
+        r = take_hi
     return out

@@ -25,9 +25,42 @@ def strong_shard(n_global: int, world: int, rank: int) -> tuple[int, int]:
     return lo, hi
 
 
-def shard_seed(config: int, rank: int, buffer: int) -> int:
-    """Data seed of a rank's buffer: disjoint across ranks and buffers."""
-    return 1000 * config + 100 * rank + buffer
+def buffer_seed(config: int, buffer: int) -> int:
+    """Base seed of rotating buffer ``buffer`` of config ``config``'s global
+    batch (buffer < 1000).  Ranks do not enter the seed: a rank holds rows
+    [lo, hi) of the global batch (``weak_shard`` / ``strong_shard``) and
+    draws exactly those rows (iqsynth.device_unit_vectors(row0=lo)), whose
+    chunk streams are distinct for every (config, buffer, chunk)."""
+    assert 0 <= buffer < 1000
+    return 1000 * config + buffer
+
+
+def plan_rows(scaling: str, n: int, world: int, rank: int) -> tuple[int, int, int]:
+    """The rows a rank streams: (row0, rows, n_global).  ``weak``: n rows per
+    rank, the global batch grows with the world; ``strong``: the global batch
+    is n rows, split contiguously (for configs[2]'s [32 layers, 8 heads,
+    32768 tokens] cache at G in {1, 2, 4, 8} this is exactly 32/G whole
+    layers per rank)."""
+    if scaling == "weak":
+        lo, hi = weak_shard(n, rank)
+        return lo, hi - lo, n * world
+    if scaling == "strong":
+        lo, hi = strong_shard(n, world, rank)
+        return lo, hi - lo, n
+    raise ValueError(scaling)
+
+
+def rank_buffers(config: int, n: int, d: int, torch_dtype, device, scaling: str = "weak",
+                 world: int = 1, rank: int = 0, buffers: int = 2):
+    """The device-resident input buffers bench.py times for one rank: for each
+    rotating buffer j, the rank's rows of config ``config``'s global batch j
+    (``plan_rows``), chunk-seeded (``buffer_seed``).  Returns (list of [rows,
+    d] tensors, row0, n_global)."""
+    import iqsynth
+    row0, rows, n_global = plan_rows(scaling, n, world, rank)
+    xs = [iqsynth.device_unit_vectors(rows, d, buffer_seed(config, j), torch_dtype, device, row0=row0)
+          for j in range(buffers)]
+    return xs, row0, n_global
 
 
 def combine_stats(step_ms: float, sq_err: float, sq_x: float, count: float, device=None):

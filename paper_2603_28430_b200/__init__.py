@@ -250,14 +250,41 @@ def _rows(x, d):
     return x.shape[0]
 
 
+def _want(t, name, shape, dtype, device):
+    """Validate a caller-supplied tensor before its pointer crosses the ABI
+    (the C side sees only pointers and n): exact shape, dtype, device and
+    contiguity, else ValueError."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected dtype {dtype}, got {t.dtype}")
+    if t.device != device:
+        raise ValueError(f"{name}: expected device {device}, got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t
+
+
+def _on_params_device(t, p: "Params", name):
+    torch = _torch()
+    if t.device.type != "cuda" or (p.device >= 0 and t.device.index != p.device):
+        raise ValueError(f"{name}: expected a tensor on cuda:{p.device}, got {t.device}")
+
+
 def iq_quantize(p: Params, x, codes=None, norms=None, stream=None):
     """x [n,d] (cuda, f32/f16) -> (codes [n, d*b/8] uint8, norms [n] f32)."""
     torch = _torch()
     n = _rows(x, p.d)
+    _on_params_device(x, p, "x")
     if codes is None:
         codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
     if norms is None:
         norms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    _want(codes, "codes", (n, p.code_bytes), torch.uint8, x.device)
+    _want(norms, "norms", (n,), torch.float32, x.device)
     _check(lib.iq_quantize(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms),
                            _stream_ptr(stream)), "iq_quantize")
     return codes, norms
@@ -266,9 +293,15 @@ def iq_quantize(p: Params, x, codes=None, norms=None, stream=None):
 def iq_dequantize(p: Params, codes, norms, dtype=None, y=None, stream=None):
     """codes [n, d*b/8] uint8 + norms [n] -> y [n, d] of ``dtype``."""
     torch = _torch()
+    if codes.dim() != 2:
+        raise ValueError(f"codes: expected [n, {p.code_bytes}], got {tuple(codes.shape)}")
     n = codes.shape[0]
+    _on_params_device(codes, p, "codes")
+    _want(codes, "codes", (n, p.code_bytes), torch.uint8, codes.device)
+    _want(norms, "norms", (n,), torch.float32, codes.device)
     if y is None:
         y = torch.empty((n, p.d), dtype=dtype or torch.float16, device=codes.device)
+    _want(y, "y", (n, p.d), dtype or y.dtype, codes.device)
     _check(lib.iq_dequantize(p.handle, _dtype_code(y), n, _ptr(codes), _ptr(norms), _ptr(y),
                              _stream_ptr(stream)), "iq_dequantize")
     return y
@@ -279,12 +312,19 @@ def iq_roundtrip(p: Params, x, y=None, codes=None, norms=None, emit_codes: bool 
     ``emit_codes`` (or codes/norms were passed)."""
     torch = _torch()
     n = _rows(x, p.d)
+    _on_params_device(x, p, "x")
     if y is None:
         y = torch.empty_like(x)
+    _want(y, "y", (n, p.d), x.dtype, x.device)
     if emit_codes and codes is None:
         codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
     if emit_codes and norms is None:
         norms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    if (codes is None) != (norms is None):
+        raise ValueError("codes and norms must be given together")
+    if codes is not None:
+        _want(codes, "codes", (n, p.code_bytes), torch.uint8, x.device)
+        _want(norms, "norms", (n,), torch.float32, x.device)
     _check(lib.iq_roundtrip(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(codes), _ptr(norms),
                             _stream_ptr(stream)), "iq_roundtrip")
     return (y, codes, norms) if codes is not None else y
@@ -295,6 +335,7 @@ def iq_quantize_qjl(p: Params, x, codes=None, norms=None, qjl=None, rnorms=None,
     stage-2 residual sketch in one kernel."""
     torch = _torch()
     n = _rows(x, p.d)
+    _on_params_device(x, p, "x")
     if codes is None:
         codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device=x.device)
     if norms is None:
@@ -303,6 +344,10 @@ def iq_quantize_qjl(p: Params, x, codes=None, norms=None, qjl=None, rnorms=None,
         qjl = torch.empty((n, iq_qjl_bytes_per_vector(p.d)), dtype=torch.uint8, device=x.device)
     if rnorms is None:
         rnorms = torch.empty((n,), dtype=torch.float32, device=x.device)
+    _want(codes, "codes", (n, p.code_bytes), torch.uint8, x.device)
+    _want(norms, "norms", (n,), torch.float32, x.device)
+    _want(qjl, "qjl", (n, iq_qjl_bytes_per_vector(p.d)), torch.uint8, x.device)
+    _want(rnorms, "rnorms", (n,), torch.float32, x.device)
     _check(lib.iq_quantize_qjl(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms), _ptr(qjl),
                                _ptr(rnorms), _stream_ptr(stream)), "iq_quantize_qjl")
     return codes, norms, qjl, rnorms
@@ -320,15 +365,25 @@ def iq_attention_scores(p: Params, codes, norms, q, qjl=None, rnorms=None, score
             qjl, rnorms = qjl.unsqueeze(0), rnorms.unsqueeze(0)
     if q.dim() == 2:
         q = q.unsqueeze(0)
+    if codes.dim() != 3 or q.dim() != 3:
+        raise ValueError("codes must be [H, N, code bytes] and q [H, n_q, d]")
     H, N = codes.shape[0], codes.shape[1]
     n_q = q.shape[1]
-    for t in (codes, norms, q) + ((qjl, rnorms) if qjl is not None else ()):
-        if not t.is_contiguous():
-            raise ValueError("tensors must be contiguous")
-    if q.shape[0] != H or q.shape[2] != p.d:
-        raise ValueError(f"q must be [{H}, n_q, {p.d}]")
+    dev = codes.device
+    _on_params_device(codes, p, "codes")
+    _want(codes, "codes", (H, N, p.code_bytes), torch.uint8, dev)
+    _want(norms, "norms", (H, N), torch.float32, dev)
+    if q.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+        raise ValueError(f"q: unsupported dtype {q.dtype}")
+    _want(q, "q", (H, n_q, p.d), q.dtype, dev)
+    if (qjl is None) != (rnorms is None):
+        raise ValueError("qjl and rnorms must be given together")
+    if qjl is not None:
+        _want(qjl, "qjl", (H, N, iq_qjl_bytes_per_vector(p.d)), torch.uint8, dev)
+        _want(rnorms, "rnorms", (H, N), torch.float32, dev)
     if scores is None:
-        scores = torch.empty((H, n_q, N), dtype=torch.float32, device=codes.device)
+        scores = torch.empty((H, n_q, N), dtype=torch.float32, device=dev)
+    _want(scores, "scores", (H, n_q, N), torch.float32, dev)
     _check(lib.iq_attention_scores(p.handle, _dtype_code(q), H, N, _ptr(codes), _ptr(norms), _ptr(qjl),
                                    _ptr(rnorms), n_q, _ptr(q), _ptr(scores), _stream_ptr(stream)),
            "iq_attention_scores")
@@ -341,10 +396,13 @@ def iq_distortion_grad(p: Params, x, grad=None, loss=None, stream=None):
     torch = _torch()
     n = _rows(x, p.d)
     nm = (4 * ((p.d + 1) // 2)) if p.variant == PLANAR2D else (16 * ((p.d + 3) // 4))
+    _on_params_device(x, p, "x")
     if grad is None:
         grad = torch.zeros(nm, dtype=torch.float64, device=x.device)
     if loss is None:
         loss = torch.zeros(1, dtype=torch.float64, device=x.device)
+    _want(grad, "grad", (nm,), torch.float64, x.device)
+    _want(loss, "loss", (1,), torch.float64, x.device)
     _check(lib.iq_distortion_grad(p.handle, _dtype_code(x), n, _ptr(x), _ptr(grad), _ptr(loss),
                                   _stream_ptr(stream)), "iq_distortion_grad")
     return grad, loss
@@ -354,8 +412,11 @@ def iq_error_sums(p: Params, x, y, sums=None, stream=None):
     """Device fp64 [sum (x-y)^2, sum x^2] (accumulated into ``sums``)."""
     torch = _torch()
     n = _rows(x, p.d)
+    _on_params_device(x, p, "x")
+    _want(y, "y", (n, p.d), x.dtype, x.device)
     if sums is None:
         sums = torch.zeros(2, dtype=torch.float64, device=x.device)
+    _want(sums, "sums", (2,), torch.float64, x.device)
     _check(lib.iq_error_sums(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(sums),
                              _stream_ptr(stream)), "iq_error_sums")
     return sums
@@ -374,7 +435,16 @@ class HostPipeline:
 
     def roundtrip(self, x_host, y_host, codes_host=None, norms_host=None):
         """x_host/y_host: CPU tensors (ideally pinned) [n, d]; synchronous."""
+        torch = _torch()
         n = _rows(x_host, self.p.d)
+        for name, t in (("x_host", x_host), ("y_host", y_host)):
+            if t.device.type != "cpu":
+                raise ValueError(f"{name}: expected a host tensor")
+        _want(y_host, "y_host", (n, self.p.d), x_host.dtype, x_host.device)
+        if codes_host is not None:
+            _want(codes_host, "codes_host", (n, self.p.code_bytes), torch.uint8, x_host.device)
+        if norms_host is not None:
+            _want(norms_host, "norms_host", (n,), torch.float32, x_host.device)
         _check(lib.iq_host_roundtrip(self._h, n, _ptr(x_host), _ptr(y_host), _ptr(codes_host),
                                      _ptr(norms_host)), "iq_host_roundtrip")
         return y_host
