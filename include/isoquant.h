@@ -123,9 +123,12 @@ iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device
  * are laid out set-major: row r of any call uses set (r / set_rows) %
  * n_sets (a KV cache [layers, heads, tokens, d] with set_rows = tokens gives
  * one set per (layer, head)); iq_attention_scores uses set h % n_sets for
- * head h.  set_rows must be a positive multiple of 256 (tiles never straddle
- * sets).  Supported by iq_quantize / iq_dequantize / iq_roundtrip / the host
- * pipeline and iq_attention_scores; not by the stage-2 sketch or the
+ * head h, iq_append_kv set r % n_sets for cache slot r.  set_rows >= 1;
+ * the batch kernels (iq_quantize / iq_dequantize / iq_roundtrip / the host
+ * pipeline) switch sets per tile and need set_rows to be a multiple of 256
+ * (else UNSUPPORTED); iq_append_kv and iq_attention_scores take any set_rows
+ * (sets finer than 256 rows, e.g. one set per (layer, head) with one row per
+ * set per decode step).  Not supported by the stage-2 sketch or the
  * distortion gradient (UNSUPPORTED / no sketch).
  */
 iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows,
@@ -275,6 +278,39 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
  * iq_rot_grad_from_operator_grad (host, chain rule to the parameters) ->
  * rot <- rot - lr * grad_rot -> iq_make_params_explicit (renormalises).
  * ------------------------------------------------------------------------ */
+
+/*
+ * iq_append_kv — quantize-on-append into a KV cache during autoregressive
+ * decoding (PAPER.md:460 / P:477, "fused KV-cache compression during
+ * autoregressive decoding").  One new row per cache
+ * slot: slot r (r = layer * heads + head for a [layers, heads, tokens, .]
+ * cache) appends row x[r] at token position pos_r:
+ *     codes bytes  [(r * cap_tokens + pos_r) * code_bytes, + code_bytes)
+ *     norms        [r * cap_tokens + pos_r]
+ *   pos_r = positions ? positions[r] : position.
+ * The layout is exactly what iq_quantize writes for the whole cache viewed
+ * as n_rows * cap_tokens rows, and row r uses parameter set r % n_sets
+ * (iq_make_params_sets; one set per (layer, head) with n_sets = n_rows), so
+ * appending tokens one at a time produces, bit for bit, the codes and norms
+ * of iq_quantize over the full cache with set_rows = cap_tokens.
+ *  dtype      : I/O dtype of x.
+ *  n_rows     : slots appended this call (n_rows = 0 is a no-op).
+ *  x          : DEVICE [n_rows, d] of dtype, 16-byte aligned.
+ *  codes      : DEVICE cache base, n_rows * cap_tokens rows of
+ *               iq_code_bytes_per_vector(d, bits) bytes, 4-byte aligned.
+ *  norms      : DEVICE fp32 cache base [n_rows * cap_tokens], 4-byte aligned.
+ *  cap_tokens : token capacity per slot (the cache's token stride), >= 1.
+ *  positions  : DEVICE int64 [n_rows] (nullable, 8-byte aligned): per-slot
+ *               positions (ragged decode batches); a position outside
+ *               [0, cap_tokens) writes nothing for that slot.
+ *  position   : the position of every slot when positions is NULL; must be
+ *               in [0, cap_tokens) (else INVALID_ARGUMENT).
+ * One kernel launch on `cuda_stream`; nothing else in the cache is touched.
+ * Errors: INVALID_ARGUMENT, MISALIGNED, UNSUPPORTED, DEVICE_MISMATCH, CUDA.
+ */
+iq_status iq_append_kv(const iq_params* p, int dtype, int64_t n_rows, const void* x, uint8_t* codes,
+                       float* norms, int64_t cap_tokens, const int64_t* positions, int64_t position,
+                       void* cuda_stream);
 
 /* Parameters from explicit rotations in the iq_export_params layout (Full
  * [g][8] = q_L, q_R; Fast [g][4]; 2D [g2][2] = (cos, sin)); each quaternion /

@@ -24,7 +24,7 @@ __all__ = [
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
     "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
     "iq_attention_scores", "iq_make_params_explicit", "iq_distortion_grad", "iq_rot_grad_from_operator_grad",
-    "iq_make_params_sets", "iq_export_params_set",
+    "iq_make_params_sets", "iq_export_params_set", "iq_append_kv",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -71,6 +71,7 @@ _sig = {
     "iq_make_params_sets": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_vp)]),
     "iq_params_sets_info": (_c_int, [_c_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_c_i64)]),
     "iq_export_params_set": (_c_int, [_c_vp, _c_int, _c_vp, _c_sz]),
+    "iq_append_kv": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -328,6 +329,26 @@ def iq_roundtrip(p: Params, x, y=None, codes=None, norms=None, emit_codes: bool 
     _check(lib.iq_roundtrip(p.handle, _dtype_code(x), n, _ptr(x), _ptr(y), _ptr(codes), _ptr(norms),
                             _stream_ptr(stream)), "iq_roundtrip")
     return (y, codes, norms) if codes is not None else y
+
+
+def iq_append_kv(p: Params, x, codes, norms, positions=None, position: int = 0, stream=None):
+    """Quantize-on-append: slot r's new row x[r] ([n_rows, d]) into the cache
+    codes [n_rows, cap, code bytes] / norms [n_rows, cap] at token
+    positions[r] (device int64 [n_rows]) or ``position``; slot r uses
+    parameter set r % n_sets.  Returns (codes, norms)."""
+    torch = _torch()
+    n = _rows(x, p.d)
+    _on_params_device(x, p, "x")
+    if codes.dim() != 3 or norms.dim() != 2:
+        raise ValueError("codes must be [n_rows, cap, code bytes] and norms [n_rows, cap]")
+    cap = codes.shape[1]
+    _want(codes, "codes", (n, cap, p.code_bytes), torch.uint8, x.device)
+    _want(norms, "norms", (n, cap), torch.float32, x.device)
+    if positions is not None:
+        _want(positions, "positions", (n,), torch.int64, x.device)
+    _check(lib.iq_append_kv(p.handle, _dtype_code(x), n, _ptr(x), _ptr(codes), _ptr(norms), cap, _ptr(positions),
+                            int(position), _stream_ptr(stream)), "iq_append_kv")
+    return codes, norms
 
 
 def iq_quantize_qjl(p: Params, x, codes=None, norms=None, qjl=None, rnorms=None, stream=None):

@@ -86,6 +86,15 @@ iq_status check_call(const iq_params* p, int dtype, int64_t n) {
   return IQ_OK;
 }
 
+// The batch stage-1 kernels switch sets per tile: tiles (<= 256 rows, every
+// tile size divides 256) must not straddle sets.
+iq_status check_batch_sets(const iq_params* p) {
+  if (p->hp.n_sets > 1 && p->hp.set_rows % 256 != 0)
+    return fail(IQ_ERR_UNSUPPORTED, "batch kernels with parameter sets need set_rows to be a multiple of 256 "
+                                    "(finer sets: iq_append_kv and iq_attention_scores)");
+  return IQ_OK;
+}
+
 iq::LaunchArgs base_args(const iq_params* p, int64_t n, void* stream) {
   iq::LaunchArgs a{};
   a.mat = p->d_mat;
@@ -190,8 +199,7 @@ iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int de
 iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows, int device,
                               iq_params** out) {
   if (n_sets < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "n_sets must be >= 1");
-  if (n_sets > 1 && (set_rows < 256 || set_rows % 256 != 0))
-    return fail(IQ_ERR_INVALID_ARGUMENT, "set_rows must be a positive multiple of 256");
+  if (n_sets > 1 && set_rows < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "set_rows must be >= 1");
   return make_params_impl(d, bits, variant, seed, device, false, out, nullptr, n_sets, set_rows);
 }
 
@@ -369,6 +377,29 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
   return run(iq::Kernel::kAttnScores, p, q_dtype, a);
 }
 
+iq_status iq_append_kv(const iq_params* p, int dtype, int64_t n_rows, const void* x, uint8_t* codes,
+                       float* norms, int64_t cap_tokens, const int64_t* positions, int64_t position,
+                       void* stream) {
+  iq_status s = check_call(p, dtype, n_rows);
+  if (s != IQ_OK) return s;
+  if (cap_tokens < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "cap_tokens must be >= 1");
+  if (!positions && (position < 0 || position >= cap_tokens))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "position must be in [0, cap_tokens)");
+  if (n_rows == 0) return IQ_OK;
+  if (!x || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "x, codes and norms are required");
+  if (!aligned(x, 16)) return fail(IQ_ERR_MISALIGNED, "x must be 16-byte aligned");
+  if (!aligned(codes, 4) || !aligned(norms, 4) || (positions && !aligned(positions, 8)))
+    return fail(IQ_ERR_MISALIGNED, "codes and norms must be 4-byte, positions 8-byte aligned");
+  iq::LaunchArgs a = base_args(p, n_rows, stream);
+  a.x = x;
+  a.codes = codes;
+  a.norms = norms;
+  a.cap = cap_tokens;
+  a.positions = positions;
+  a.position = position;
+  return run(iq::Kernel::kAppend, p, dtype, a);
+}
+
 iq_status iq_distortion_grad(const iq_params* p, int dtype, int64_t n, const void* x, double* grad, double* loss,
                              void* stream) {
   iq_status s = check_call(p, dtype, n);
@@ -389,6 +420,7 @@ iq_status iq_quantize(const iq_params* p, int dtype, int64_t n, const void* x, u
                       float* norms, void* stream) {
   iq_status s = check_call(p, dtype, n);
   if (s != IQ_OK) return s;
+  if ((s = check_batch_sets(p)) != IQ_OK) return s;
   if (n == 0) return IQ_OK;
   if (!x || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "x, codes and norms are required");
   if (!aligned(x, 16)) return fail(IQ_ERR_MISALIGNED, "x must be 16-byte aligned");
@@ -405,6 +437,7 @@ iq_status iq_dequantize(const iq_params* p, int dtype, int64_t n, const uint8_t*
                         const float* norms, void* y, void* stream) {
   iq_status s = check_call(p, dtype, n);
   if (s != IQ_OK) return s;
+  if ((s = check_batch_sets(p)) != IQ_OK) return s;
   if (n == 0) return IQ_OK;
   if (!y || !codes || !norms) return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms and y are required");
   if (!aligned(y, 16) || !aligned(codes, 16) || !aligned(norms, 16))
@@ -420,6 +453,7 @@ iq_status iq_roundtrip(const iq_params* p, int dtype, int64_t n, const void* x, 
                        uint8_t* codes, float* norms, void* stream) {
   iq_status s = check_call(p, dtype, n);
   if (s != IQ_OK) return s;
+  if ((s = check_batch_sets(p)) != IQ_OK) return s;
   if (n == 0) return IQ_OK;
   if (!x || !y) return fail(IQ_ERR_INVALID_ARGUMENT, "x and y are required");
   if ((codes == nullptr) != (norms == nullptr))
@@ -501,6 +535,7 @@ iq_status iq_host_pipeline_create(const iq_params* p, int dtype, int64_t chunk_v
   iq_status s = check_call(p, dtype, 0);
   if (s != IQ_OK) return s;
   if (chunk_vectors <= 0) return fail(IQ_ERR_INVALID_ARGUMENT, "chunk_vectors must be > 0");
+  if ((s = check_batch_sets(p)) != IQ_OK) return s;
   if (p->hp.n_sets > 1 && chunk_vectors % (p->hp.set_rows * p->hp.n_sets) != 0)
     return fail(IQ_ERR_INVALID_ARGUMENT, "with parameter sets, chunk_vectors must be a multiple of set_rows * n_sets");
   iq_host_pipeline* pl = new (std::nothrow) iq_host_pipeline();

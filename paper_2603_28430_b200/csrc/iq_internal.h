@@ -124,9 +124,13 @@ struct LaunchArgs {
   const uint8_t* qjl_img;   // device UMMA image of S (stage 2)
   uint8_t* qjl;             // [n, d/8] sketch sign bits (stage 2)
   float* rnorms;            // [n] residual norms (stage 2)
+  // quantize-on-append (k_append): cache of n rows x cap tokens
+  int64_t cap;
+  const int64_t* positions; // device [n] or null (then `position` for every row)
+  int64_t position;
 };
 
-enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5, kDistortionGrad = 6 };
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5, kDistortionGrad = 6, kAppend = 7 };
 
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.

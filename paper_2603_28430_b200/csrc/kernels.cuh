@@ -110,7 +110,9 @@ constexpr int pick_cpl() {
 }
 
 // Kernel kinds: 0 quantize (K1), 1 fused roundtrip (K3), 2 fused roundtrip +
-// codes, 3 dequantize (K2).  Coordinates per lane (TPL), measured on B200
+// codes, 3 dequantize (K2), 4 distortion gradient, 5 quantize-on-append (K1's
+// lane geometry, so it emits K1's codes and norms bit for bit; operators in
+// registers because every lane group may use a different parameter set).  Coordinates per lane (TPL), measured on B200
 // (DESIGN.md section 6): 16 for every encoder except the fp32 code-emitting
 // ones (8); K1 and K3+codes share one geometry so that they emit
 // bit-identical codes and norms; the decoder 8.
@@ -139,7 +141,7 @@ constexpr int pick_tpl() {
 // fused kernel, and for the fp32 quantizer; registers (8 warps) otherwise.
 template <class T, int BITS, int KIND>
 constexpr bool pick_ops_smem() {
-  if (!IQ_OPS_SMEM || KIND >= 3) return false;
+  if (!IQ_OPS_SMEM || KIND >= 3) return false;   // decoder, gradient, append: registers
   if (sizeof(T) == 2) return !(KIND == 1 && BITS <= 2);
   return KIND == 0;
 }
@@ -771,6 +773,132 @@ __device__ __forceinline__ void ring_init(uint64_t* full, uint64_t* empty) {
   }
 }
 
+// Stage 1 for one pair of rows once their norms are known (Alg.1 l.2-18):
+// forward rotation, the decision, and -- per MODE -- the code words of each
+// chunk (cwa / cwb: row A / row B) and / or the reconstruction x^ (out).
+// Shared by the batch encoders (k_encode) and the append kernel (k_append),
+// so both take bit-identical decisions.  v: the rows' coordinate pairs, ss:
+// their squared norms before the lane-group reduction is applied to rho.
+template <class T, int D, int BITS, int VAR, int MODE, int KIND = MODE>
+__device__ __forceinline__ void encode_pair(
+    const float2 (&v)[Geo<T, D, BITS, VAR, KIND>::EPL], float2 ss, float2 rho,
+    const float (&P)[Geo<T, D, BITS, VAR, KIND>::OPS_SMEM ? 1 : Geo<T, D, BITS, VAR, KIND>::NBL]
+                    [Geo<T, D, BITS, VAR, KIND>::PW * Geo<T, D, BITS, VAR, KIND>::PW],
+    const uint8_t* ops, int sub, const KCodebook& cb, float ctab, float gtab, float gval, uint32_t gcode,
+    float2 (&out)[Geo<T, D, BITS, VAR, KIND>::EPL], uint32_t (&cwa)[Geo<T, D, BITS, VAR, KIND>::CPL],
+    uint32_t (&cwb)[Geo<T, D, BITS, VAR, KIND>::CPL]) {
+  using Gm = Geo<T, D, BITS, VAR, KIND>;
+  constexpr int EPC = Gm::EPC, CPL = Gm::CPL, PW = Gm::PW, NBL = Gm::NBL;
+  constexpr bool emit = MODE != 1;
+  constexpr bool value = MODE != 0;
+  constexpr bool GRID = BITS >= IQ_GRID_MIN_BITS;          // uniform-grid decision [R19]
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
+  if constexpr (GRID) {
+    // u = |T x| * S / max(rho, eps): the normalisation (Alg.1 l.1) and
+    // the power-of-two grid scale enter as the FFMAs' multiplier [R19]
+    const float2 sc = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)) * cb.gscale,
+                         rsqrt_ftz(fmaxf(ss.y, 1e-24f)) * cb.gscale);
+#pragma unroll
+    for (int b = 0; b < NBL; ++b) {
+      float2 yb[PW], cq[PW];
+      float Mb[PW * PW];
+      fetch_op<Gm>(P, ops, sub, b, Mb);
+      rot_fwd<PW>(Mb, v + b * PW, yb);               // T(x)  (Alg.1 l.5/9/13)
+#pragma unroll
+      for (int j = 0; j < PW; ++j) {
+        const uint32_t ia = grid_index(yb[j].x, sc.x, gtab, cb.gclamp);
+        const uint32_t ib = grid_index(yb[j].y, sc.y, gtab, cb.gclamp);
+        if constexpr (emit) {
+          const int e = (b * PW + j) % EPC, c = (b * PW + j) / EPC;
+          cwa[c] |= grid_code<BITS>(ia, yb[j].x, gcode) << (e * BITS);
+          cwb[c] |= grid_code<BITS>(ib, yb[j].y, gcode) << (e * BITS);
+        }
+        if constexpr (value)                         // v^ = C[code] (sign restored)
+          cq[j] = f2(grid_value(ia, yb[j].x, gval), grid_value(ib, yb[j].y, gval));
+      }
+      if constexpr (value) {
+        rot_inv<PW>(Mb, cq, out + b * PW);           // T^-1 (l.7/11/15)
+#pragma unroll
+        for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);   // x^ = rho * ...
+      }
+    }
+  } else {
+  // Decision rule (R14c).  SCALED: compare y = T(x) with per-row
+  // thresholds r*tau, r = max(rho, eps) (saves normalising the row).
+  // K1 (MODE 0) and K3+codes (MODE 2) always use it, so they emit
+  // identical codes; MODE 2 then looks C[code] up in a shuffle table and
+  // rescales after T^-1.  The value-only K3 (MODE 1) also builds
+  // rho*C[code] directly (no rescale) for b <= 3; for b = 4 (seven
+  // thresholds, register-bound) it normalises the row and compares with
+  // the codebook as stored.
+  constexpr bool SCALED = MODE != 1 || BITS <= 3;
+  constexpr bool RESCALE = value && !SCALED;
+  RowQ<BITS> q;
+  float2 inv = bc(1.0f);
+  if constexpr (SCALED) {
+    make_rowq<BITS, MODE == 1>(q, rho, cb);
+  } else {
+    inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
+  }
+
+  if constexpr (!emit) {                             // K3: values only
+#pragma unroll
+    for (int b = 0; b < NBL; ++b) {
+      float2 yb[PW], cq[PW];
+      float Mb[PW * PW];
+      fetch_op<Gm>(P, ops, sub, b, Mb);
+      if constexpr (SCALED) {
+        rot_fwd<PW>(Mb, v + b * PW, yb);           // y = T(x)  (Alg.1 l.5/9/13, [R14c])
+      } else {
+        float2 xb[PW];
+#pragma unroll
+        for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
+        rot_fwd<PW>(Mb, xb, yb);                     // v~ = T(xbar)
+      }
+#pragma unroll
+      for (int j = 0; j < PW; ++j) {
+        uint32_t d0, d1;
+        if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
+        else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
+      }
+      rot_inv<PW>(Mb, cq, out + b * PW);             // x^ = T^-1(rho * v^)  (l.7/11/15)
+      if constexpr (RESCALE) {
+#pragma unroll
+        for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
+      }
+    }
+  } else {                                           // K1 / K3+codes
+    constexpr int BPCH = EPC / PW;                   // blocks per chunk
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      float2 yb[EPC];
+      float Mc[BPCH][PW * PW];
+#pragma unroll
+      for (int bb = 0; bb < BPCH; ++bb) {
+        fetch_op<Gm>(P, ops, sub, i * BPCH + bb, Mc[bb]);
+        rot_fwd<PW>(Mc[bb], v + i * EPC + bb * PW, yb + bb * PW);             // y = T(x)
+      }
+      encode_chunk<BITS, EPC>(yb, q, cwa[i], cwb[i]);                       // codes of Q(y)
+      if constexpr (value) {
+        float2 cq[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC; ++e)                // v^ = C[code], width-L shuffle table
+          cq[e] = f2(__shfl_sync(kFull, ctab, (int)(cwa[i] >> (e * BITS)), 1 << BITS),
+                     __shfl_sync(kFull, ctab, (int)(cwb[i] >> (e * BITS)), 1 << BITS));
+#pragma unroll
+        for (int bb = 0; bb < BPCH; ++bb) {
+          float2* o = out + i * EPC + bb * PW;
+          rot_inv<PW>(Mc[bb], cq + bb * PW, o);             // T^-1
+#pragma unroll
+          for (int j = 0; j < PW; ++j) o[j] = mul2(o[j], rho);   // x^ = rho * ...
+        }
+      }
+    }
+  }
+  }  // !GRID
+}
+
 // --------------------------------------------------------- encoder (K1/K3)
 // MODE 0: quantize (codes + norms).  MODE 1: fused roundtrip (y only).
 // MODE 2: fused roundtrip that also writes codes and norms.
@@ -835,7 +963,6 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
   constexpr bool emit = MODE != 1;
   constexpr bool value = MODE != 0;
   const float ctab = cb.cent[lane & ((1 << BITS) - 1)];   // C[k] in lane k of each group of L
-  constexpr bool GRID = BITS >= IQ_GRID_MIN_BITS;          // uniform-grid decision [R19]
   const float gtab = cb.gtab[lane];
   const float gval = cb.gval[lane];
   const uint32_t gcode = cb.gcode[lane];
@@ -896,111 +1023,7 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
       float2 out[EPL];
       uint32_t cwa[CPL], cwb[CPL];
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) cwa[i] = cwb[i] = 0u;
-      if constexpr (GRID) {
-        // u = |T x| * S / max(rho, eps): the normalisation (Alg.1 l.1) and
-        // the power-of-two grid scale enter as the FFMAs' multiplier [R19]
-        const float2 sc = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)) * cb.gscale,
-                             rsqrt_ftz(fmaxf(ss.y, 1e-24f)) * cb.gscale);
-#pragma unroll
-        for (int b = 0; b < NBL; ++b) {
-          float2 yb[PW], cq[PW];
-          float Mb[PW * PW];
-          fetch_op<Gm>(P, ops, sub, b, Mb);
-          rot_fwd<PW>(Mb, v + b * PW, yb);               // T(x)  (Alg.1 l.5/9/13)
-#pragma unroll
-          for (int j = 0; j < PW; ++j) {
-            const uint32_t ia = grid_index(yb[j].x, sc.x, gtab, cb.gclamp);
-            const uint32_t ib = grid_index(yb[j].y, sc.y, gtab, cb.gclamp);
-            if constexpr (emit) {
-              const int e = (b * PW + j) % EPC, c = (b * PW + j) / EPC;
-              cwa[c] |= grid_code<BITS>(ia, yb[j].x, gcode) << (e * BITS);
-              cwb[c] |= grid_code<BITS>(ib, yb[j].y, gcode) << (e * BITS);
-            }
-            if constexpr (value)                         // v^ = C[code] (sign restored)
-              cq[j] = f2(grid_value(ia, yb[j].x, gval), grid_value(ib, yb[j].y, gval));
-          }
-          if constexpr (value) {
-            rot_inv<PW>(Mb, cq, out + b * PW);           // T^-1 (l.7/11/15)
-#pragma unroll
-            for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);   // x^ = rho * ...
-          }
-        }
-      } else {
-      // Decision rule (R14c).  SCALED: compare y = T(x) with per-row
-      // thresholds r*tau, r = max(rho, eps) (saves normalising the row).
-      // K1 (MODE 0) and K3+codes (MODE 2) always use it, so they emit
-      // identical codes; MODE 2 then looks C[code] up in a shuffle table and
-      // rescales after T^-1.  The value-only K3 (MODE 1) also builds
-      // rho*C[code] directly (no rescale) for b <= 3; for b = 4 (seven
-      // thresholds, register-bound) it normalises the row and compares with
-      // the codebook as stored.
-      constexpr bool SCALED = MODE != 1 || BITS <= 3;
-      constexpr bool RESCALE = value && !SCALED;
-      RowQ<BITS> q;
-      float2 inv = bc(1.0f);
-      if constexpr (SCALED) {
-        make_rowq<BITS, MODE == 1>(q, rho, cb);
-      } else {
-        inv = f2(rsqrt_ftz(fmaxf(ss.x, 1e-24f)), rsqrt_ftz(fmaxf(ss.y, 1e-24f)));   // 1/max(rho, eps)
-      }
-
-      if constexpr (!emit) {                             // K3: values only
-#pragma unroll
-        for (int b = 0; b < NBL; ++b) {
-          float2 yb[PW], cq[PW];
-          float Mb[PW * PW];
-          fetch_op<Gm>(P, ops, sub, b, Mb);
-          if constexpr (SCALED) {
-            rot_fwd<PW>(Mb, v + b * PW, yb);           // y = T(x)  (Alg.1 l.5/9/13, [R14c])
-          } else {
-            float2 xb[PW];
-#pragma unroll
-            for (int j = 0; j < PW; ++j) xb[j] = mul2(v[b * PW + j], inv);   // xbar (l.1)
-            rot_fwd<PW>(Mb, xb, yb);                     // v~ = T(xbar)
-          }
-#pragma unroll
-          for (int j = 0; j < PW; ++j) {
-            uint32_t d0, d1;
-            if constexpr (SCALED) cq[j] = quantize_pair<BITS, true, false>(yb[j], q, d0, d1);
-            else cq[j] = quantize_pair_u<BITS, true, false>(yb[j], cb, d0, d1);
-          }
-          rot_inv<PW>(Mb, cq, out + b * PW);             // x^ = T^-1(rho * v^)  (l.7/11/15)
-          if constexpr (RESCALE) {
-#pragma unroll
-            for (int j = 0; j < PW; ++j) out[b * PW + j] = mul2(out[b * PW + j], rho);
-          }
-        }
-      } else {                                           // K1 / K3+codes
-        constexpr int BPCH = EPC / PW;                   // blocks per chunk
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-          float2 yb[EPC];
-          float Mc[BPCH][PW * PW];
-#pragma unroll
-          for (int bb = 0; bb < BPCH; ++bb) {
-            fetch_op<Gm>(P, ops, sub, i * BPCH + bb, Mc[bb]);
-            rot_fwd<PW>(Mc[bb], v + i * EPC + bb * PW, yb + bb * PW);             // y = T(x)
-          }
-          encode_chunk<BITS, EPC>(yb, q, cwa[i], cwb[i]);                       // codes of Q(y)
-          if constexpr (value) {
-            float2 cq[EPC];
-#pragma unroll
-            for (int e = 0; e < EPC; ++e)                // v^ = C[code], width-L shuffle table
-              cq[e] = f2(__shfl_sync(kFull, ctab, (int)(cwa[i] >> (e * BITS)), 1 << BITS),
-                         __shfl_sync(kFull, ctab, (int)(cwb[i] >> (e * BITS)), 1 << BITS));
-#pragma unroll
-            for (int bb = 0; bb < BPCH; ++bb) {
-              float2* o = out + i * EPC + bb * PW;
-              rot_inv<PW>(Mc[bb], cq + bb * PW, o);             // T^-1
-#pragma unroll
-              for (int j = 0; j < PW; ++j) o[j] = mul2(o[j], rho);   // x^ = rho * ...
-            }
-          }
-        }
-      }
-      }  // !GRID
+      encode_pair<T, D, BITS, VAR, MODE>(v, ss, rho, P, ops, sub, cb, ctab, gtab, gval, gcode, out, cwa, cwb);
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         if constexpr (value) {
@@ -1026,6 +1049,76 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
       }
     }
   }
+}
+
+
+// ------------------------------------------- quantize-on-append (KV cache)
+// One new row per cache slot r (a (layer, head) pair, r = layer * heads +
+// head) quantized straight into a strided cache during decoding (P:460,
+// P:477): codes row r * cap + pos_r (RB bytes), norms[r * cap + pos_r], with
+// the operators of parameter set r % n_sets [R31] and K1's lane geometry and
+// decision code (encode_pair), so the codes and norms are bit-identical to
+// iq_quantize of the same row with the same set.  One lane group per row,
+// rows read with 128-bit loads (a decode step moves a few hundred rows: the
+// kernel is latency-bound, not a bandwidth kernel).  A lane group whose row
+// does not exist mirrors the last row (its shuffles need the whole warp) and
+// stores nothing; a position outside [0, cap) stores nothing.
+template <class T, int D, int BITS, int VAR>
+__global__ void __launch_bounds__(256)
+k_append(const float* __restrict__ mat, const KCodebook cb, int64_t n_rows, const T* __restrict__ x,
+         uint8_t* __restrict__ codes, float* __restrict__ norms, int64_t cap, const int64_t* __restrict__ positions,
+         int64_t position) {
+  using Gm = Geo<T, D, BITS, VAR, 5>;
+  constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW, PW = Gm::PW, NBL = Gm::NBL;
+  constexpr int EPL = Gm::EPL, B = Gm::B, W = Gm::W, RB = Gm::RB;
+  static_assert(!Gm::OPS_SMEM, "append: operators in registers");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane & (G - 1), vbase = lane & ~(G - 1), vslot = lane / G;
+  const int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * VPW + vslot;
+  if (((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * VPW >= n_rows) return;   // warp-uniform
+  const int64_t rr = r < n_rows ? r : n_rows - 1;
+  const int64_t pos = positions ? positions[rr] : position;
+  const bool store = r < n_rows && pos >= 0 && pos < cap;
+  const int set = cb.n_sets > 1 ? (int)(rr % cb.n_sets) : 0;
+  float P[NBL][PW * PW];
+  load_ops<Gm>(mat + (size_t)set * cb.set_stride, sub, P);
+  const T* xr = x + rr * D;
+  uint4 ra[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) ra[i] = __ldg(reinterpret_cast<const uint4*>(xr + (sub + i * G) * EPC));
+  float2 v[EPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) to_pairs<T>(ra[i], ra[i], v + i * EPC);
+  // Alg.1 l.1: rho = ||x||_2, in k_encode's summation order
+#if IQ_NORM_SPLIT
+  float2 ss = mul2(v[0], v[0]), ss1 = mul2(v[1], v[1]);
+#pragma unroll
+  for (int e = 2; e < EPL; e += 2) {
+    ss = fma2(v[e], v[e], ss);
+    ss1 = fma2(v[e + 1], v[e + 1], ss1);
+  }
+  ss = add2(ss, ss1);
+#else
+  float2 ss = mul2(v[0], v[0]);
+#pragma unroll
+  for (int e = 1; e < EPL; ++e) ss = fma2(v[e], v[e], ss);
+#endif
+#pragma unroll
+  for (int o = G / 2; o >= 1; o >>= 1)
+    ss = add2(ss, f2(__shfl_xor_sync(kFull, ss.x, o), __shfl_xor_sync(kFull, ss.y, o)));
+  const float2 rho = f2(sqrt_ftz(ss.x), sqrt_ftz(ss.y));
+  const float ctab = cb.cent[lane & ((1 << BITS) - 1)];
+  float2 out[EPL];
+  uint32_t cwa[CPL], cwb[CPL];
+  encode_pair<T, D, BITS, VAR, 0, 5>(v, ss, rho, P, nullptr, sub, cb, ctab, cb.gtab[lane], cb.gval[lane],
+                                     cb.gcode[lane], out, cwa, cwb);
+  uint8_t* cr = codes + (rr * cap + pos) * RB;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const uint32_t w = gather_word<G, B>(cwa[i], sub, vbase);
+    if (store && sub < W) *reinterpret_cast<uint32_t*>(cr + 4 * (i * W + sub)) = w;
+  }
+  if (store && sub == 0) norms[rr * cap + pos] = rho.x;
 }
 
 // ---------------------------------------------------------------- decoder (K2)

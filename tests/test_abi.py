@@ -152,7 +152,10 @@ def test_param_sets_generator_matches_oracle(iq):
         assert np.array_equal(iq.iq_export_params_set(p, s), want)
         qL, qR, _ = O.make_rotation_params(64, O.FULL, 20260331 + s)
         assert np.allclose(want.reshape(-1, 8)[:, :4], qL, atol=1e-15)
+    # any set_rows >= 1 (finer sets serve iq_append_kv / the consumer; the
+    # batch kernels refuse them at call time, tests/test_gpu_append.py)
+    iq.iq_make_params_sets(64, 3, iq.FULL, 1, 2, 100, device=-1)
     with pytest.raises(iq.IQError):
-        iq.iq_make_params_sets(64, 3, iq.FULL, 1, 2, 100, device=-1)     # set_rows % 256 != 0
+        iq.iq_make_params_sets(64, 3, iq.FULL, 1, 2, 0, device=-1)       # set_rows < 1
     with pytest.raises(iq.IQError):
         iq.iq_export_params_set(p, 3)
