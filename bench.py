@@ -585,7 +585,7 @@ def kernel_entries(torch, iq, iqsynth, a, p, xs, ys, n, vid, dev, stream, peak, 
                                 "bytes_per_launch": b, "vectors_per_s": n / (t / 1e3),
                                 "tensor_tflops": n * 4 * a.d * a.d / (t / 1e3) / 1e12}
         del qj, rn
-    if a.d in (64, 128) and n >= 32 * 1024:   # fused KV-cache decode consumer (NEXT row 2), the batch as keys
+    if n >= 32 * 1024:   # fused KV-cache decode consumer (NEXT row 2), the batch as keys
         H = 32                                  # heads of n/32 keys each, 4 queries per head (GQA)
         nk = n // H
         qh = torch.randn((H, 4, a.d), dtype=xs[0].dtype, device=dev)

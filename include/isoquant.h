@@ -261,7 +261,10 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
  *  q      : [heads, n_q, d] of q_dtype      scores : [heads, n_q, n_keys] float
  * Precision: fp16 centroids and queries (per-query power-of-two scaling):
  * |error| <= ~1e-3 * rho_hk * ||q_hj|| (stage 1), see DESIGN.md.  d in
- * {64, 128}.  codes, norms, qjl, rnorms 16-byte aligned; with heads > 1,
+ * {64, 128, 256, 512} (d > 128: the key tile's operand is built and
+ * accumulated in 128-coordinate chunks); the stage-2 term needs d in
+ * {64, 128} (UNSUPPORTED otherwise).  Head h uses parameter set h % n_sets.
+ * codes, norms, qjl, rnorms 16-byte aligned; with heads > 1,
  * n_keys % 4 == 0 (else MISALIGNED).
  */
 iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_t n_keys,

@@ -63,16 +63,25 @@ def _compile(src: str, extra: list[str], verbose: bool, objdir: str = OBJDIR) ->
 
 
 def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | None = None,
-          lib: str = LIB, objdir: str = OBJDIR) -> str:
+          lib: str = LIB, objdir: str = OBJDIR, only: list[str] | None = None) -> str:
     """Compile (incrementally) and link libisoquant.so; return its path.
     ``extra``/``lib``/``objdir`` build tuning variants (e.g. -DIQ_NWC=7) side by
-    side for experiments; the product is the default build."""
+    side for experiments; the product is the default build.  ``only``: the
+    source basenames compiled with ``extra`` into ``objdir``; every other
+    translation unit links the product build's object (a variant of one
+    kernel family rebuilds one file)."""
     os.makedirs(objdir, exist_ok=True)
     extra = list(extra or [])
     srcs = _sources()
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
+
+    def one(src):
+        if only is not None and os.path.basename(src) not in only:
+            return _compile(src, [], verbose, OBJDIR)
+        return _compile(src, extra, verbose, objdir)
+
     with ThreadPoolExecutor(max_workers=jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra, verbose, objdir), srcs))
+        objs = list(ex.map(one, srcs))
     if not os.path.exists(lib) or os.path.getmtime(lib) < _newest(objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-cudart", "static"]
         if verbose:

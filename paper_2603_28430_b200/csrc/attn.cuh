@@ -36,21 +36,28 @@ struct AGeo {
   static constexpr int NQ = 16;                  // query slots (UMMA N)
   static constexpr int TILE = 128;               // keys per tile (UMMA M)
   static constexpr int RB = D * BITS / 8;        // code bytes per key
-  static constexpr int QB = D / 8;               // sketch bytes per key
+  // K-split: the A operand of a tile is built and consumed in chunks of KCH
+  // coordinates (one 128 x KCH fp16 K-major operand each, accumulated into
+  // one TMEM accumulator), so d = 256 / 512 keys fit the same buffers
+  static constexpr int KCH = D < 128 ? D : 128;
+  static constexpr int KC = D / KCH;             // chunks per tile
+  static constexpr bool ST2OK = D <= 128;        // stage-2 term (the sketch kernel's widths)
+  static constexpr int NPART = ST2OK ? 2 : 1;    // A parts per buffer: stage 1 [, stage 2]
+  static constexpr int QB = ST2OK ? D / 8 : 0;   // sketch bytes per key
   // ring stage: codes [TILE][RB] | norms [TILE] | sketch [TILE][QB] | gammas [TILE]
   static constexpr int C_OFF = 0;
   static constexpr int N_OFF = (TILE * RB + 15) / 16 * 16;
   static constexpr int Q_OFF = N_OFF + TILE * 4;
   static constexpr int G_OFF = Q_OFF + TILE * QB;
-  static constexpr int STAGE = (G_OFF + TILE * 4 + 127) / 128 * 128;
-  static constexpr int A_BYTES = TILE * D * 2;   // one fp16 A tile
-  static constexpr int B_BYTES = NQ * D * 2;     // one fp16 B tile (queries)
+  static constexpr int STAGE = (G_OFF + (ST2OK ? TILE * 4 : 0) + 127) / 128 * 128;
+  static constexpr int A_BYTES = TILE * KCH * 2; // one fp16 A operand chunk
+  static constexpr int B_BYTES = NQ * D * 2;     // one fp16 B tile (queries, all of K)
   static constexpr int S_BYTES = 128 * D * 2;    // S as a 128-row A operand (staged in the A buffers)
-  static constexpr int A_OFF = 0;                // [2 buffers][stage 1, stage 2]
-  static constexpr int B_OFF = A_OFF + 4 * A_BYTES;
-  static constexpr int QT_OFF = B_OFF + 2 * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
+  static constexpr int A_OFF = 0;                // [2 buffers][NPART]
+  static constexpr int B_OFF = A_OFF + 2 * NPART * A_BYTES;
+  static constexpr int QT_OFF = B_OFF + NPART * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
   static constexpr int NACC = 4;                 // accumulator / side-table buffers (TMEM is cheap)
-  static constexpr int SIDE_OFF = QT_OFF + B_BYTES;    // per accumulator: rho[128], gamma[128], scales[2][16]
+  static constexpr int SIDE_OFF = QT_OFF + (ST2OK ? B_BYTES : 0);   // per accumulator: rho[128], gamma[128], scales[2][16]
   static constexpr int SIDE_BYTES = (2 * TILE + 2 * NQ) * 4;
   static constexpr int QS_OFF = SIDE_OFF + NACC * SIDE_BYTES;   // the current head's scales [2][16]
   // lookup tables replicated across the 32 banks (entry e of lane l at
@@ -59,7 +66,7 @@ struct AGeo {
   static constexpr int PAIRS = 1 << (2 * BITS);
   static constexpr int PT_OFF = QS_OFF + 2 * NQ * 4;
   static constexpr int ST_OFF = PT_OFF + PAIRS * 128;
-  static constexpr int BAR_OFF = ST_OFF + 16 * 256;
+  static constexpr int BAR_OFF = ST_OFF + (ST2OK ? 16 * 256 : 0);
   static constexpr int RING_OFF = (BAR_OFF + 512 + 127) / 128 * 128;
   static constexpr int RING_MAX = 227 * 1024 - RING_OFF - 1024;
   static constexpr int NST = (RING_MAX / STAGE) < 16 ? (RING_MAX / STAGE) : 16;
@@ -71,12 +78,12 @@ struct AGeo {
   static constexpr int NWE = 4;                  // epilogue warps (one per TMEM lane quadrant)
   static constexpr int W_PROD = NWD + NWE, W_MMA = NWD + NWE + 1;
   static constexpr int CTA_THREADS = 32 * (NWD + NWE + 2);
-  static constexpr int GROUPS = D / 32;          // 32-coordinate groups per key
+  static constexpr int CGROUPS = KCH / 32;       // 32-coordinate groups per key and chunk
   static constexpr int TMEM_COLS = 256;          // [NACC][stage 1, stage 2] x NQ, + NQ for S q
   static constexpr int SQ_COL = 2 * NACC * NQ;
-  static_assert(D == 64 || D == 128, "attention consumer: d in {64, 128}");
+  static_assert(D == 64 || D == 128 || D == 256 || D == 512, "attention consumer: d in {64, 128, 256, 512}");
   static_assert(NST >= 3, "ring too shallow");
-  static_assert(S_BYTES <= 4 * A_BYTES, "S staging");
+  static_assert(!ST2OK || S_BYTES <= 4 * A_BYTES, "S staging");
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -96,14 +103,14 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
               const uint8_t* __restrict__ s_img, int n_q, const TQ* __restrict__ q, float* __restrict__ scores) {
   using A = AGeo<D, BITS>;
   constexpr int TILE = A::TILE, NQ = A::NQ, NWD = A::NWD, NST = A::NST, RB = A::RB, QB = A::QB;
-  constexpr int GROUPS = A::GROUPS;
+  constexpr int KC = A::KC, KCH = A::KCH, NPART = A::NPART, CGROUPS = A::CGROUPS;
   constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;
   constexpr int L = 1 << BITS;
-  const bool st2 = sketch != nullptr;
+  const bool st2 = A::ST2OK && sketch != nullptr;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* a_base = smem + A::A_OFF;            // A[buf][part] at a_base + (2 buf + part) A_BYTES
+  uint8_t* a_base = smem + A::A_OFF;            // A[buf][part] at a_base + (NPART buf + part) A_BYTES
   uint8_t* b_base = smem + A::B_OFF;            // B[part]
   float* qs = reinterpret_cast<float*>(smem + A::QS_OFF);   // [2][NQ]: 1/sigma_j, 8/sigma_j
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
@@ -179,22 +186,26 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
       const uint32_t ab = smem_u32(a_base), bb = smem_u32(b_base);
-      uint32_t j = 0;
+      uint32_t j = 0, jj = 0;                    // tiles, A-operand chunks
       for (int64_t t = t_begin; t < t_end; ++t, ++j) {
-        const uint32_t b = j & 1, c = j % A::NACC, u = j / A::NACC;
-        mbar_wait_tc(&a_full[b], (j >> 1) & 1);
+        const uint32_t c = j % A::NACC, u = j / A::NACC;
         mbar_wait_tc(&acc_empty[c], (u & 1) ^ 1);
-        tc_fence_after();
 #pragma unroll 1
-        for (int part = 0; part < (st2 ? 2 : 1); ++part) {
-          const uint32_t ta = ab + (2 * b + part) * A::A_BYTES, tb = bb + part * A::B_BYTES;
-          const uint32_t td = tmem + (2 * c + part) * NQ;
+        for (int kc = 0; kc < KC; ++kc, ++jj) {
+          const uint32_t b = jj & 1;
+          mbar_wait_tc(&a_full[b], (jj >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int part = 0; part < (st2 ? 2 : 1); ++part) {
+            const uint32_t ta = ab + (NPART * b + part) * A::A_BYTES, tb = bb + part * A::B_BYTES;
+            const uint32_t td = tmem + (2 * c + part) * NQ;
 #pragma unroll
-          for (int s = 0; s < D / 16; ++s)
-            umma_f16(td, umma_desc_sw128(ta + umma_kstep_off(s, TILE)), umma_desc_sw128(tb + umma_kstep_off(s, NQ)),
-                     idesc, s != 0);
+            for (int s = 0; s < KCH / 16; ++s)
+              umma_f16(td, umma_desc_sw128(ta + umma_kstep_off(s, TILE)),
+                       umma_desc_sw128(tb + umma_kstep_off(kc * (KCH / 16) + s, NQ)), idesc, (kc | s) != 0);
+          }
+          umma_commit(&a_free[b]);
         }
-        umma_commit(&a_free[b]);
         umma_commit(&acc_full[c]);
       }
     }
@@ -246,7 +257,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const __half2 hv = __floats2half2_rn(cb.cent[pr & (L - 1)], cb.cent[pr >> BITS]);
       *reinterpret_cast<__half2*>(smem + A::PT_OFF + pr * 128 + 4 * l) = hv;
     }
-    for (int e = threadIdx.x; e < 16 * 32; e += NWD * 32) {   // bit set = +1 (R22)
+    for (int e = threadIdx.x; A::ST2OK && e < 16 * 32; e += NWD * 32) {   // bit set = +1 (R22); stage 2 only
       const int nib = e >> 5, l = e & 31;
       uint32_t w[2];
 #pragma unroll
@@ -266,7 +277,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     auto load_queries = [&](int64_t h) {
       const TQ* qh = q + h * (int64_t)n_q * D;
       const float* mset = mat + (size_t)(h % cb.n_sets) * cb.set_stride;   // the head's set [R31]
-      if (st2 && threadIdx.x == 0) {             // stage S in the drained A buffers
+      if (A::ST2OK && st2 && threadIdx.x == 0) {   // stage S in the drained A buffers
         mbar_arrive_expect_tx(s_bar, A::S_BYTES);
         bulk_g2s(a_base, s_img, A::S_BYTES, s_bar, policy_evict_last());
       }
@@ -305,7 +316,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         for (int r = 0; r < PW; ++r)
           *reinterpret_cast<__half*>(b_base + umma_sw128_off(jq, b * PW + r, NQ)) = __float2half_rn(yv[r]);
       }
-      if (st2) {
+      if (A::ST2OK && st2) {
         // stage 2: S q on the tensor cores.  B = sigma q as fp16 (queries x d),
         // A = S (128 x d, rows >= m zero), D = S (sigma q)^T in TMEM; thread i
         // of warps 0..3 then holds (S sigma q_j)_i for the 16 query slots and
@@ -350,31 +361,31 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
     };
 
     __builtin_assume(threadIdx.x < NWD * 32);
-    // per-thread constants of the decode mapping (thread g -> key g / GROUPS,
-    // 32-coordinate group g % GROUPS): stage word offsets, A-tile chunk offsets
-    constexpr int NG = (TILE * GROUPS + NWD * 32 - 1) / (NWD * 32);   // groups per thread
+    // per-thread constants of the decode mapping (thread g -> key g / CGROUPS,
+    // 32-coordinate group g % CGROUPS of every chunk): stage word offsets
+    // (chunk 0), A-operand chunk offsets
+    constexpr int NG = (TILE * CGROUPS + NWD * 32 - 1) / (NWD * 32);   // groups per thread and chunk
     uint32_t coff[NG], qoff[NG], aoff[NG][4];
 #pragma unroll
     for (int gi = 0; gi < NG; ++gi) {
       const int g = threadIdx.x + gi * NWD * 32;
-      const int gr = g / GROUPS, gs = g % GROUPS;
+      const int gr = g / CGROUPS, gs = g % CGROUPS;
       coff[gi] = (uint32_t)(gr * RB + gs * BITS * 4);
-      qoff[gi] = (uint32_t)(gr * QB + gs * 4);
+      qoff[gi] = (uint32_t)(gr * A::QB + gs * 4);
 #pragma unroll
       for (int c8 = 0; c8 < 4; ++c8) aoff[gi][c8] = umma_sw128_off(gr, gs * 32 + c8 * 8, TILE);
     }
     int s = 0;
-    uint32_t ph = 0, j = 0;
+    uint32_t ph = 0, j = 0, jj = 0;
     int64_t hcur = -1;
     float qs_mine = 0.0f;                        // qs[threadIdx.x] of the current head (threads < 2 NQ)
     int64_t h = t_begin / tph, k0 = (t_begin - h * tph) * TILE;
     for (int64_t t = t_begin; t < t_end; ++t, ++j, k0 += TILE) {
       if (k0 >= n_keys) { k0 = 0; ++h; }
-      const uint32_t b = j & 1;
       if (h != hcur) {
-        // drain: the last MMA issued (tile j - 1) completes after every
+        // drain: the last MMA issued (chunk jj - 1) completes after every
         // earlier one, so the B tiles and both A buffers are free
-        if (j > 0) mbar_wait_tc(&a_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        if (jj > 0) mbar_wait_tc(&a_free[(jj - 1) & 1], ((jj - 1) >> 1) & 1);
         load_queries(h);
         hcur = h;
         if (threadIdx.x < 2 * NQ) qs_mine = qs[threadIdx.x];
@@ -386,39 +397,51 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       const int64_t nk = (n_keys - k0) < TILE ? (n_keys - k0) : TILE;
       const int64_t hrow0 = h * n_keys + k0;
       const uint32_t cb16 = (uint32_t)(nk * RB) & ~15u, nb16 = (uint32_t)(nk * 4) & ~15u;
-      const uint32_t qb16 = (uint32_t)(nk * QB) & ~15u;
+      const uint32_t qb16 = (uint32_t)(nk * A::QB) & ~15u;
       const bool full_tile = nk == TILE;         // TILE * (RB, 4, QB) are 16-byte multiples
-      // decode mapping: thread g -> (key gr = g / GROUPS, group gs = g % GROUPS)
-      // of 32 coordinates: BITS code words and one sketch word, contiguous in
-      // the stage (consecutive lanes read consecutive words: no bank conflicts)
-      uint32_t cw[NG][BITS], sw[NG];
+      // every chunk's code words (BITS per 32-coordinate group) and sketch
+      // words, contiguous in the stage (consecutive lanes read consecutive
+      // words: no bank conflicts); the stage is released once they are in
+      uint32_t cw[KC][NG][BITS], sw[NG];
       float dep = 0.0f;
 #pragma unroll
-      for (int gi = 0; gi < NG; ++gi) {
-        const int g = threadIdx.x + gi * NWD * 32;
-        const int gr = g / GROUPS, gs = g % GROUPS;
-        const bool gv = g < TILE * GROUPS && gr < nk;
-        if (full_tile && g < TILE * GROUPS) {   // everything is in the stage
+      for (int kc = 0; kc < KC; ++kc) {
 #pragma unroll
-          for (int i = 0; i < BITS; ++i) cw[gi][i] = lds32(stg + A::C_OFF + coff[gi] + 4 * i);
-          sw[gi] = st2 ? lds32(stg + A::Q_OFF + qoff[gi]) : 0u;
-        } else {
+        for (int gi = 0; gi < NG; ++gi) {
+          const int g = threadIdx.x + gi * NWD * 32;
+          const int gr = g / CGROUPS, gs = kc * CGROUPS + g % CGROUPS;
+          const bool gv = g < TILE * CGROUPS && gr < nk;
+          if (full_tile && g < TILE * CGROUPS) {   // everything is in the stage
 #pragma unroll
-          for (int i = 0; i < BITS; ++i) {
-            const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
-            cw[gi][i] = !gv ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
-                                                      : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
+            for (int i = 0; i < BITS; ++i) cw[kc][gi][i] = lds32(stg + A::C_OFF + coff[gi] + kc * (CGROUPS * BITS * 4) + 4 * i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BITS; ++i) {
+              const uint32_t off = (uint32_t)(gr * RB + (gs * BITS + i) * 4);
+              cw[kc][gi][i] = !gv ? 0u : (off + 4 <= cb16) ? lds32(stg + A::C_OFF + off)
+                                                            : __ldg(reinterpret_cast<const uint32_t*>(codes + hrow0 * RB + off));
+            }
           }
-          sw[gi] = 0u;
-          if (st2) {
-            const uint32_t off = (uint32_t)(gr * QB + gs * 4);
-            sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
-                                                   : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * QB + off));
-          }
+#pragma unroll
+          for (int i = 0; i < BITS; ++i) dep += __uint_as_float(cw[kc][gi][i] & 0x007FFFFFu);
         }
+      }
 #pragma unroll
-        for (int i = 0; i < BITS; ++i) dep += __uint_as_float(cw[gi][i] & 0x007FFFFFu);
-        dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
+      for (int gi = 0; gi < NG; ++gi) {
+        sw[gi] = 0u;
+        if (A::ST2OK && st2) {
+          const int g = threadIdx.x + gi * NWD * 32;
+          const int gr = g / CGROUPS, gs = g % CGROUPS;
+          const bool gv = g < TILE * CGROUPS && gr < nk;
+          if (full_tile && g < TILE * CGROUPS) {
+            sw[gi] = lds32(stg + A::Q_OFF + qoff[gi]);
+          } else {
+            const uint32_t off = (uint32_t)(gr * A::QB + gs * 4);
+            sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
+                                                   : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * A::QB + off));
+          }
+          dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
+        }
       }
       // rho and gamma of the tile's keys for the side table
       float rg = 0.0f;
@@ -432,7 +455,6 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_after(&empty[ss_], dep);
-      mbar_wait_tc(&a_free[b], ((j >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of tile j - 2
       const uint32_t ca = j % A::NACC;
       mbar_wait_tc(&acc_empty[ca], ((j / A::NACC) & 1) ^ 1);   // side table read by the epilogue of tile j - NACC
       float* side = reinterpret_cast<float*>(smem + A::SIDE_OFF + ca * A::SIDE_BYTES);
@@ -442,53 +464,57 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         __syncwarp();
         if (lane == 0) mbar_arrive(&side_full[ca]);
       }
-      uint8_t* a1 = a_base + (2 * b) * A::A_BYTES;
-      uint8_t* a2 = a1 + A::A_BYTES;
 #pragma unroll
-      for (int gi = 0; gi < NG; ++gi) {
-        const int g = threadIdx.x + gi * NWD * 32;
-        if (g >= TILE * GROUPS) continue;
-        const int gr = g / GROUPS, gs = g % GROUPS;
-        // stage 1: C[code] as fp16, two coordinates per lookup: the pair's
-        // 2 BITS-bit field is shifted to bit 7 and OR-ed into this lane's
-        // column of the pair table (one SHF + LOP3 + LDS per pair)
+      for (int kc = 0; kc < KC; ++kc, ++jj) {
+        const uint32_t b = jj & 1;
+        mbar_wait_tc(&a_free[b], ((jj >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of chunk jj - 2
+        uint8_t* a1 = a_base + (NPART * b) * A::A_BYTES;
+        uint8_t* a2 = a1 + A::A_BYTES;
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
-          uint32_t hw[4];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const int b0 = (c8 * 8 + e) * BITS;
-            constexpr uint32_t MSK = (uint32_t)(A::PAIRS - 1) << 7;
-            uint32_t f;
-            if (b0 % 32 + 2 * BITS <= 32) {
-              const int sh = b0 % 32 - 7;
-              f = sh >= 0 ? (cw[gi][b0 / 32] >> sh) : (cw[gi][b0 / 32] << -sh);
-            } else {
-              f = __funnelshift_r(cw[gi][b0 / 32], cw[gi][b0 / 32 + 1], b0 % 32) << 7;
-            }
-            hw[e / 2] = lds32_addr(((f & MSK) | pt_lane) + pt_base);
-          }
-          *reinterpret_cast<uint4*>(a1 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        }
-        if (st2) {  // stage 2: +-1 from the sketch bits, four per lookup
+        for (int gi = 0; gi < NG; ++gi) {
+          const int g = threadIdx.x + gi * NWD * 32;
+          if (g >= TILE * CGROUPS) continue;
+          // stage 1: C[code] as fp16, two coordinates per lookup: the pair's
+          // 2 BITS-bit field is shifted to bit 7 and OR-ed into this lane's
+          // column of the pair table (one SHF + LOP3 + LDS per pair)
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             uint32_t hw[4];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int b0 = c8 * 8 + 4 * e;
-              const uint32_t f = b0 >= 8 ? (sw[gi] >> (b0 - 8)) : (sw[gi] << (8 - b0));
-              const uint2 t2 = lds64_addr(((f & (15u << 8)) | st_lane) + st_base);
-              hw[2 * e] = t2.x;
-              hw[2 * e + 1] = t2.y;
+            for (int e = 0; e < 8; e += 2) {
+              const int b0 = (c8 * 8 + e) * BITS;
+              constexpr uint32_t MSK = (uint32_t)(A::PAIRS - 1) << 7;
+              uint32_t f;
+              if (b0 % 32 + 2 * BITS <= 32) {
+                const int sh = b0 % 32 - 7;
+                f = sh >= 0 ? (cw[kc][gi][b0 / 32] >> sh) : (cw[kc][gi][b0 / 32] << -sh);
+              } else {
+                f = __funnelshift_r(cw[kc][gi][b0 / 32], cw[kc][gi][b0 / 32 + 1], b0 % 32) << 7;
+              }
+              hw[e / 2] = lds32_addr(((f & MSK) | pt_lane) + pt_base);
             }
-            *reinterpret_cast<uint4*>(a2 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(a1 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          }
+          if (A::ST2OK && st2) {  // stage 2: +-1 from the sketch bits, four per lookup
+#pragma unroll
+            for (int c8 = 0; c8 < 4; ++c8) {
+              uint32_t hw[4];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int b0 = c8 * 8 + 4 * e;
+                const uint32_t f = b0 >= 8 ? (sw[gi] >> (b0 - 8)) : (sw[gi] << (8 - b0));
+                const uint2 t2 = lds64_addr(((f & (15u << 8)) | st_lane) + st_base);
+                hw[2 * e] = t2.x;
+                hw[2 * e + 1] = t2.y;
+              }
+              *reinterpret_cast<uint4*>(a2 + aoff[gi][c8]) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            }
           }
         }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[b]);
       }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[b]);
     }
   }
   tc_fence_before();

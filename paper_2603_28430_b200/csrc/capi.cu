@@ -23,7 +23,7 @@ int launch_full_bf16(Kernel, int, int, const LaunchArgs&);
 int launch_fast_bf16(Kernel, int, int, const LaunchArgs&);
 int launch_planar2d_bf16(Kernel, int, int, const LaunchArgs&);
 
-bool attn_supported(int d) { return d == 64 || d == 128; }
+bool attn_supported(int d) { return d == 64 || d == 128 || d == 256 || d == 512; }
 
 bool gpu_supported(int d, int bits, int variant) {
   const bool dok = d == 64 || d == 128 || d == 256 || d == 512;
@@ -349,13 +349,15 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
   iq_status s = check_call(p, q_dtype, n_keys);
   if (s != IQ_OK) return s;
   if (!iq::attn_supported(p->hp.d))
-    return fail(IQ_ERR_UNSUPPORTED, "the attention consumer supports d in {64, 128}");
+    return fail(IQ_ERR_UNSUPPORTED, "the attention consumer supports d in {64, 128, 256, 512}");
   if (heads < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "heads must be >= 1");
   if (n_q < 1 || n_q > 16) return fail(IQ_ERR_INVALID_ARGUMENT, "n_q must be in [1, 16]");
   if ((qjl == nullptr) != (rnorms == nullptr))
     return fail(IQ_ERR_INVALID_ARGUMENT, "qjl and rnorms must be both NULL or both set");
   if (qjl && (!p->hp.has_qjl || !p->d_qjl_a))
     return fail(IQ_ERR_INVALID_ARGUMENT, "stage-2 scores need a handle with the sketch (iq_make_params_qjl)");
+  if (qjl && p->hp.d > 128)
+    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 term of the consumer supports d in {64, 128}");
   if (n_keys == 0) return IQ_OK;
   if (!codes || !norms || !q || !scores)
     return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms, q and scores are required");

@@ -135,7 +135,7 @@ enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums =
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.
 int launch(Kernel k, int variant, int dtype, int d, int bits, const LaunchArgs& a);
-bool attn_supported(int d);   // attention consumer: d in {64, 128}
+bool attn_supported(int d);   // attention consumer: d in {64, 128, 256, 512} (stage 2: 64, 128)
 bool gpu_supported(int d, int bits, int variant);
 
 }  // namespace iq

@@ -78,6 +78,32 @@ def test_attn_grid(bits, d, dt, stage2):
     _run(d, bits, iq.FULL, dt, heads=2, n_keys=1024 + 4 * bits, n_q=4, stage2=stage2, seed=bits)
 
 
+@pytest.mark.parametrize("dt", [iq.F16, iq.F32])
+@pytest.mark.parametrize("variant", [iq.FULL, iq.FAST, iq.PLANAR2D])
+@pytest.mark.parametrize("d", [256, 512])
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_attn_wide_heads(bits, d, variant, dt):
+    """d in {256, 512} (the paper's widths): the key tile's A operand
+    is built and accumulated in 128-coordinate chunks (stage 1)."""
+    _run(d, bits, variant, dt, heads=3, n_keys=700 + 4 * bits, n_q=5, stage2=False, seed=d + bits)
+
+
+@pytest.mark.parametrize("n_keys", [1, 129, 4100])
+def test_attn_wide_shapes_and_head_switches(n_keys):
+    _run(512, 4, iq.FULL, iq.F16, heads=1, n_keys=n_keys, n_q=16, stage2=False, seed=n_keys)
+    _run(256, 3, iq.FAST, iq.F16, heads=300, n_keys=128, n_q=4, stage2=False, seed=3)
+
+
+def test_attn_wide_stage2_unsupported():
+    p = iq.iq_make_params(256, 3, iq.FULL, SEED, device=0)
+    codes = torch.zeros((1, 8, 96), dtype=torch.uint8, device="cuda")
+    norms = torch.zeros((1, 8), dtype=torch.float32, device="cuda")
+    qjl = torch.zeros((1, 8, 32), dtype=torch.uint8, device="cuda")
+    q = torch.zeros((1, 2, 256), dtype=torch.float16, device="cuda")
+    with pytest.raises(iq.IQError):
+        iq.iq_attention_scores(p, codes, norms, q, qjl, norms.clone())
+
+
 @pytest.mark.parametrize("variant", [iq.FAST, iq.PLANAR2D])
 def test_attn_variants(variant):
     _run(128, 3, variant, iq.F16, heads=3, n_keys=600, n_q=8, stage2=True, seed=11)

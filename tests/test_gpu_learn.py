@@ -1,10 +1,15 @@
 """GPU parity of the distortion-gradient kernel (iq_distortion_grad, R29)
-against the fp64 oracle, and a short learning loop through the C ABI
-(GPU gradient -> host chain rule -> explicit parameters).  Tolerance:
-Frobenius-relative 1e-3 on dL/dM (fp32 per-row math; a decision taken on the
-other side of a threshold -- allowed for 1e-4 of coordinates -- moves that
-row's contribution by 2 dC xbar, which is large against the small b = 4
-gradient) and 1e-4 on the distortion."""
+against the fp64 oracle, element by element, and a short learning loop
+through the C ABI (GPU gradient -> host chain rule -> explicit parameters).
+
+Per-element tolerance on dL/dM_b[i][j] = 2 sum_rows e_i xbar_j, derived from
+the arithmetic: (1) the kernel's fp32 row math (normalisation, rotation,
+e = ybar - C[code]) carries ~1e-6 relative error on each product, so
+5e-5 * 2 sum_rows |e_i| |xbar_j| bounds the accumulated rounding; (2) a
+decision taken on the other side of a threshold (the parity bar allows it
+within 1e-5 of a threshold) moves that row's e_i by the centroid gap dC, so
+every oracle coordinate within 1e-5 of a threshold adds 2 dC |xbar_j| to its
+elements' allowance.  The distortion agrees to 1e-4 relative."""
 import numpy as np
 import pytest
 
@@ -35,9 +40,17 @@ def test_grad_parity(bits, d, variant, dt):
     grad, loss = iq.iq_distortion_grad(p, torch.from_numpy(X).cuda())
     torch.cuda.synchronize()
     po = O.make_params(d, bits, variant, SEED)
-    Go = Lo.operator_grad(X, po).reshape(-1)
-    Gg = grad.cpu().numpy()
-    assert np.linalg.norm(Gg - Go) <= 1e-3 * np.linalg.norm(Go), np.linalg.norm(Gg - Go) / np.linalg.norm(Go)
+    Go = Lo.operator_grad(X, po)
+    Gg = grad.cpu().numpy().reshape(Go.shape)
+    xb, yb, e = Lo._blocks(X, po)
+    scale = 2.0 * np.einsum("ngi,ngj->gij", np.abs(e), np.abs(xb))
+    T = po.cb.thresholds
+    near = np.min(np.abs(yb[..., None] - T), axis=-1) <= 1e-5              # [n, g, w]
+    gap = float(np.max(np.diff(po.cb.centroids)))
+    flip = 2.0 * gap * np.einsum("ngi,ngj->gij", near.astype(np.float64), np.abs(xb))
+    err = np.abs(Gg - Go)
+    tol = 5e-5 * scale + flip + 1e-12
+    assert np.all(err <= tol), float(np.max(err / tol))
     Lw = Lo.distortion(X, po)
     assert abs(float(loss) - Lw) <= 1e-4 * Lw
 

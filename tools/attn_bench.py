@@ -20,7 +20,9 @@ def main():
     import torch, iqsynth
     import paper_2603_28430_b200 as iq
     n = a.heads * a.keys
-    p = iq.iq_make_params_qjl(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
+    st2 = a.d <= 128                      # the stage-2 sketch exists for d in {64, 128}
+    mk = iq.iq_make_params_qjl if st2 else iq.iq_make_params
+    p = mk(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
     codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device="cuda")
     norms = torch.empty(n, dtype=torch.float32, device="cuda")
     qj = torch.empty((n, a.d // 8), dtype=torch.uint8, device="cuda")
@@ -29,7 +31,10 @@ def main():
     for r0 in range(0, n, chunk):
         m = min(chunk, n - r0)
         x = iqsynth.device_unit_vectors(m, a.d, 9000 + r0 // chunk, torch.float16, "cuda")
-        iq.iq_quantize_qjl(p, x, codes[r0:r0 + m], norms[r0:r0 + m], qj[r0:r0 + m], rn[r0:r0 + m])
+        if st2:
+            iq.iq_quantize_qjl(p, x, codes[r0:r0 + m], norms[r0:r0 + m], qj[r0:r0 + m], rn[r0:r0 + m])
+        else:
+            iq.iq_quantize(p, x, codes[r0:r0 + m], norms[r0:r0 + m])
     del x
     q = torch.randn((a.heads, a.nq, a.d), dtype=torch.float16, device="cuda")
     scores = torch.empty((a.heads, a.nq, a.keys), dtype=torch.float32, device="cuda")
@@ -40,7 +45,7 @@ def main():
         ("stage1", lambda: iq.iq_attention_scores(p, c3, n3, q, scores=scores), p.code_bytes + 4 + 4 * a.nq),
         ("stage1+2", lambda: iq.iq_attention_scores(p, c3, n3, q, q3, r3, scores=scores),
          p.code_bytes + 4 + a.d // 8 + 4 + 4 * a.nq),
-    ]:
+    ][:2 if st2 else 1]:
         for _ in range(3):
             fn()
         torch.cuda.synchronize()

@@ -44,6 +44,9 @@ VARIANTS = {
     "qjl1mma": ["-DIQ_QJL_PASSES=1"],       # timing probe only: one MMA pass (inexact sketch)
     "qjlnowait": ["-DIQ_QJL_NOWAIT_PROBE=1"],   # timing probe only: A tile reuse without the MMA wait (racy)
     "norotd": ["-DIQ_QJL_ROTD=0"],          # stage 2 residual in the input domain (2 passes)
+    "pu2": ["-DIQ_PAIR_UNROLL=2"],          # two row pairs per loop iteration (operator fetch shared)
+    "b3fma64": ["-DIQ_B3_ALU=0", "-DIQ_STAGE_KB=64"],
+    "b3fmapu2": ["-DIQ_B3_ALU=0", "-DIQ_PAIR_UNROLL=2"],
 }
 
 
@@ -51,12 +54,12 @@ def lib_path(name):
     return os.path.join(ROOT, "paper_2603_28430_b200", "build", f"var_{name}", "libisoquant.so")
 
 
-def build(names):
+def build(names, only=None):
     from __graft_entry__ import load_builder
     _build = load_builder()
     for name in names:
         d = os.path.dirname(lib_path(name))
-        _build.build(extra=VARIANTS[name], lib=lib_path(name), objdir=d)
+        _build.build(extra=VARIANTS[name], lib=lib_path(name), objdir=d, only=only)
         print("built", name, flush=True)
 
 
@@ -67,7 +70,8 @@ def time_one(a):
     tdt = torch.float16 if a.dtype == "f16" else torch.float32
     s = 2 if a.dtype == "f16" else 4
     p = iq.iq_make_params(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
-    xs = [iqsynth.device_unit_vectors(a.n, a.d, 7 + j, tdt, "cuda") for j in range(2)]
+    from iqsynth import dist as D
+    xs, _, _ = D.rank_buffers(2, a.n, a.d, tdt, "cuda", buffers=2)
     ys = [torch.empty_like(x) for x in xs]
     codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
     norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
@@ -86,17 +90,30 @@ def time_one(a):
          2 * a.d * s + cb + 4),
     ] + ([("qjl", lambda i: iq.iq_quantize_qjl(pq, xs[i & 1], codes, norms, qj, rn), a.d * s + cb + 8 + a.d // 8)]
          if a.d in (64, 128) else []):
+        if a.kernels and name not in a.kernels:
+            continue
         for i in range(5):
             fn(i)
         torch.cuda.synchronize()
+        if a.sustained:                       # the bench protocol: settle under load, then time
+            import time as _t
+            t0 = _t.time()
+            i = 0
+            while _t.time() - t0 < a.sustained:
+                fn(i)
+                i += 1
+                if i % 64 == 0:
+                    torch.cuda.synchronize()
+            torch.cuda.synchronize()
+        reps = 200 if a.sustained else 40
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(40):
+        for i in range(reps):
             fn(i)
         e1.record()
         torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) / 40 * 1e3
-        out[name] = (round(us, 1), round(a.n * bpv / us / 1e3 / 6525.9, 3))
+        us = e0.elapsed_time(e1) / reps * 1e3
+        out[name] = (round(us, 1), round(a.n * bpv / us / 1e3 / 6545.0, 3))
     print(json.dumps(out))
 
 
@@ -109,9 +126,13 @@ def main():
     ap.add_argument("--dtype", default="f16")
     ap.add_argument("--variant", default="full")
     ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--sustained", type=float, default=0.0,
+                    help="seconds of untimed settle load before timing (the bench protocol)")
+    ap.add_argument("--kernels", nargs="*", default=None, help="subset of rt q dq rte qjl")
+    ap.add_argument("--tu", nargs="*", default=None, help="build: only these translation units (basenames)")
     a = ap.parse_args()
     if a.cmd == "build":
-        build(a.only)
+        build(a.only, a.tu)
     elif a.cmd == "time1":
         time_one(a)
     else:
@@ -120,7 +141,8 @@ def main():
                 continue
             env = dict(os.environ, IQ_LIB_PATH=lib_path(name))
             r = subprocess.run([sys.executable, __file__, "time1", "--d", str(a.d), "--bits", str(a.bits),
-                                "--dtype", a.dtype, "--variant", a.variant, "--n", str(a.n)],
+                                "--dtype", a.dtype, "--variant", a.variant, "--n", str(a.n),
+                                "--sustained", str(a.sustained)] + (["--kernels"] + a.kernels if a.kernels else []),
                                env=env, capture_output=True, text=True)
             line = (r.stdout.strip().splitlines() or [r.stderr.strip()[-300:]])[-1]
             print(f"{name:16s} {line}", flush=True)
