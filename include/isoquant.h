@@ -220,8 +220,9 @@ iq_status iq_roundtrip(const iq_params* p, int dtype, int64_t n, const void* x,
  *      x~ = x^ + sqrt(pi/2)/m * gamma * S^T q  (unbiased over S).
  * ------------------------------------------------------------------------ */
 
-/* iq_make_params plus the stage-2 sketch S (m = d).  The GPU sketch kernel
- * supports d in {64, 128} (UNSUPPORTED otherwise when device >= 0). */
+/* iq_make_params plus the stage-2 sketch S (m = d).  The GPU sketch path
+ * supports d in {64, 128, 256, 512} -- the paper's head widths
+ * (UNSUPPORTED otherwise when device >= 0). */
 iq_status iq_make_params_qjl(int d, int bits, int variant, uint64_t seed, int device,
                              iq_params** out);
 
@@ -234,12 +235,16 @@ size_t iq_qjl_bytes_per_vector(int d);
 iq_status iq_export_qjl_matrix(const iq_params* p, float* S, size_t len);
 
 /*
- * iq_quantize_qjl — stage 1 + stage 2 in one kernel: x[n,d] -> codes, norms
- * (bit-identical to iq_quantize), qjl[n, d/8] sign bits of S r and
- * rnorms[n] = ||r||.  One persistent kernel: TMA ring for x, the stage-1
+ * iq_quantize_qjl — stage 1 + stage 2: x[n,d] -> codes, norms (bit-identical
+ * to iq_quantize), qjl[n, d/8] sign bits of S r and rnorms[n] = ||r||.
+ * d in {64, 128}: one persistent kernel -- TMA ring for x, the stage-1
  * encoder in CUDA cores, r split into fp16 hi + lo tiles in shared memory,
  * z = S (r_hi + r_lo) on the tensor cores (tcgen05.mma, fp32 accumulators in
- * TMEM), sign packing from TMEM.  x 16-byte aligned; codes, norms, rnorms
+ * TMEM), sign packing from TMEM.  d in {256, 512} (S no longer fits shared
+ * memory): two launches on the stream -- the iq_quantize kernel, then a
+ * sketch kernel that reads x, the codes and the norms back, rebuilds r
+ * K-chunk by K-chunk and streams S from L2 through shared memory (same
+ * arithmetic, same readings).  x 16-byte aligned; codes, norms, rnorms
  * 4-byte and qjl 8-byte aligned.
  */
 iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* x,

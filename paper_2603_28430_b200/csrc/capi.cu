@@ -150,7 +150,7 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
   }
   if (qjl && device >= 0 && !iq::qjl_supported(d)) {
     delete p;
-    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 sketch kernel supports d in {64, 128}");
+    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 sketch kernels support d in {64, 128, 256, 512}");
   }
   p->device = device;
   if (device >= 0) {
@@ -168,11 +168,13 @@ static iq_status make_params_impl(int d, int bits, int variant, uint64_t seed, i
     if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl, p->hp.qjl_img.size());
     if (e == cudaSuccess && qjl)
       e = cudaMemcpy(p->d_qjl, p->hp.qjl_img.data(), p->hp.qjl_img.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl_rot, p->hp.qjl_img_rot.size());
-    if (e == cudaSuccess && qjl)
+    // the rotated-domain and attention images exist for the fused d <= 128 kernels only
+    const bool rot = qjl && !p->hp.qjl_img_rot.empty(), aimg = qjl && !p->hp.qjl_img_a.empty();
+    if (e == cudaSuccess && rot) e = cudaMalloc(&p->d_qjl_rot, p->hp.qjl_img_rot.size());
+    if (e == cudaSuccess && rot)
       e = cudaMemcpy(p->d_qjl_rot, p->hp.qjl_img_rot.data(), p->hp.qjl_img_rot.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && qjl) e = cudaMalloc(&p->d_qjl_a, p->hp.qjl_img_a.size());
-    if (e == cudaSuccess && qjl)
+    if (e == cudaSuccess && aimg) e = cudaMalloc(&p->d_qjl_a, p->hp.qjl_img_a.size());
+    if (e == cudaSuccess && aimg)
       e = cudaMemcpy(p->d_qjl_a, p->hp.qjl_img_a.data(), p->hp.qjl_img_a.size(), cudaMemcpyHostToDevice);
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -340,7 +342,12 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
   a.qjl_img_rot = p->d_qjl_rot;
   a.qjl = qjl;
   a.rnorms = rnorms;
-  return run(iq::Kernel::kQuantizeQjl, p, dtype, a);
+  if (iq::qjl_fused(p->hp.d)) return run(iq::Kernel::kQuantizeQjl, p, dtype, a);
+  // d in {256, 512}: the stage-1 quantizer, then the sketch kernel reading
+  // back x, the codes and the norms (two launches on the caller's stream)
+  s = run(iq::Kernel::kQuantize, p, dtype, a);
+  if (s != IQ_OK) return s;
+  return run(iq::Kernel::kQjlSketch, p, dtype, a);
 }
 
 iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_t n_keys,
@@ -354,10 +361,10 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
   if (n_q < 1 || n_q > 16) return fail(IQ_ERR_INVALID_ARGUMENT, "n_q must be in [1, 16]");
   if ((qjl == nullptr) != (rnorms == nullptr))
     return fail(IQ_ERR_INVALID_ARGUMENT, "qjl and rnorms must be both NULL or both set");
-  if (qjl && (!p->hp.has_qjl || !p->d_qjl_a))
-    return fail(IQ_ERR_INVALID_ARGUMENT, "stage-2 scores need a handle with the sketch (iq_make_params_qjl)");
   if (qjl && p->hp.d > 128)
     return fail(IQ_ERR_UNSUPPORTED, "the stage-2 term of the consumer supports d in {64, 128}");
+  if (qjl && (!p->hp.has_qjl || !p->d_qjl_a))
+    return fail(IQ_ERR_INVALID_ARGUMENT, "stage-2 scores need a handle with the sketch (iq_make_params_qjl)");
   if (n_keys == 0) return IQ_OK;
   if (!codes || !norms || !q || !scores)
     return fail(IQ_ERR_INVALID_ARGUMENT, "codes, norms, q and scores are required");

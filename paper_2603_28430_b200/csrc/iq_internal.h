@@ -73,7 +73,8 @@ bool add_param_sets(HostParams* hp, int n_sets, int64_t set_rows, std::string* e
 
 // Sketch generator key and layout (params.cpp).
 bool build_qjl(HostParams* hp, std::string* err);
-bool qjl_supported(int d);   // GPU sketch kernel: d in {64, 128}
+bool qjl_supported(int d);   // GPU sketch: d in {64, 128} (fused kernel), {256, 512} (quantize + sketch kernel)
+bool qjl_fused(int d);       // d in {64, 128}: one fused stage-1 + sketch kernel
 // byte offset of element (row r, k) in a K-major 128B-swizzled UMMA operand
 // with `rows` rows: K slabs of 64 fp16, 8-row atoms of 1024 B
 #ifdef __CUDACC__
@@ -130,7 +131,7 @@ struct LaunchArgs {
   int64_t position;
 };
 
-enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5, kDistortionGrad = 6, kAppend = 7 };
+enum class Kernel { kQuantize = 0, kDequantize = 1, kRoundtrip = 2, kErrorSums = 3, kQuantizeQjl = 4, kAttnScores = 5, kDistortionGrad = 6, kAppend = 7, kQjlSketch = 8 };
 
 // Dispatch to the template instance for (kernel, variant, dtype, d, bits).
 // Returns: 0 ok, -1 unsupported configuration, else the CUDA error code.

@@ -60,8 +60,14 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_NWC_WIDE
 #define IQ_NWC_WIDE 16       // compute warps of the wide encoder CTAs
 #endif
+#ifndef IQ_NWC_NARROW
+#define IQ_NWC_NARROW 8      // compute warps of the encoder CTAs with operators in registers
+#endif
 #ifndef IQ_B3_ALU
 #define IQ_B3_ALU 1          // b = 3 fused value chain: FSETP + predicated FADD (else FSET + FFMA2)
+#endif
+#ifndef IQ_FHADD
+#define IQ_FHADD 0           // fp16 -> fp32 with the mixed-precision FHADD (else HADD2.F32)
 #endif
 #ifndef IQ_PAIR_UNROLL
 #define IQ_PAIR_UNROLL 1
@@ -87,7 +93,17 @@ template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, f
 // the packed 16-bit pair of T -> two floats (exact)
 template <class T> __device__ __forceinline__ float2 unpack2(uint32_t w);
 template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
+#if IQ_FHADD
+  // mixed-precision add f32 = f16 + (-0.0f): exact, one full-rate FMA-pipe
+  // slot per value (HADD2.F32 takes two)
+  float a, b;
+  asm("{.reg .b16 l, h; mov.b32 {l, h}, %2;\n"
+      "add.rn.f32.f16 %0, l, 0f80000000; add.rn.f32.f16 %1, h, 0f80000000;}"
+      : "=f"(a), "=f"(b) : "r"(w));
+  return make_float2(a, b);
+#else
   return __half22float2(*reinterpret_cast<const __half2*>(&w));
+#endif
 }
 template <> __device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
@@ -163,7 +179,7 @@ struct Geo {
   // 16 compute warps fit the register file
   static constexpr bool OPS_SMEM = ENC && !SMALL_OPS && pick_ops_smem<T, BITS, KIND>();
   static constexpr bool WIDE = ENC && (SMALL_OPS || OPS_SMEM);
-  static constexpr int NWC = WIDE ? IQ_NWC_WIDE : 8;               // compute warps per CTA
+  static constexpr int NWC = WIDE ? IQ_NWC_WIDE : (ENC ? IQ_NWC_NARROW : 8);   // compute warps per CTA
   static constexpr int CTA_THREADS = 32 * (NWC + 1);               // + 1 producer warp
   static constexpr int MIN_CTAS = (ENC || !SMALL_OPS) ? 1 : 2;
   static constexpr int OPS_BYTES = OPS_SMEM ? G * NBL * PW * PW * 4 : 0;

@@ -415,7 +415,8 @@ uint16_t half_rn(double x) {
 }
 }  // namespace
 
-bool qjl_supported(int d) { return d == 64 || d == 128; }
+bool qjl_fused(int d) { return d == 64 || d == 128; }
+bool qjl_supported(int d) { return qjl_fused(d) || d == 256 || d == 512; }
 
 bool build_qjl(HostParams* hp, std::string* err) {
   const int d = hp->d, m = d;
@@ -433,14 +434,14 @@ bool build_qjl(HostParams* hp, std::string* err) {
         std::memcpy(&hp->qjl_img[umma_sw128_off(i, k, m)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
   }
   hp->qjl_img_a.clear();
-  if (qjl_supported(d)) {
+  if (qjl_fused(d)) {
     hp->qjl_img_a.assign(static_cast<size_t>(128) * d * 2, 0);
     for (int i = 0; i < m; ++i)
       for (int k = 0; k < d; ++k)
         std::memcpy(&hp->qjl_img_a[umma_sw128_off(i, k, 128)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
   }
   hp->qjl_img_rot.clear();
-  if (qjl_supported(d)) {
+  if (qjl_fused(d)) {
     const int pw = hp->variant == IQ_VARIANT_PLANAR2D ? 2 : 4;
     const size_t img = static_cast<size_t>(m) * d * 2;
     hp->qjl_img_rot.assign(2 * img, 0);

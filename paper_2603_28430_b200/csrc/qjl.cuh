@@ -32,6 +32,9 @@ struct QGeo {
 #ifndef IQ_QJL_NOWAIT_PROBE
 #define IQ_QJL_NOWAIT_PROBE 0   // timing probe only: compute warps do not wait for the A tile (racy)
 #endif
+#ifndef IQ_QJL_TCWAIT
+#define IQ_QJL_TCWAIT 0   // compute-warp waits on tcgen05.commit barriers without a suspend hint
+#endif
 #ifndef IQ_QJL_PASSES
 #define IQ_QJL_PASSES (Q::ROTD ? 3 : 2)   // MMA passes per tile (timing probes override it)
 #endif
@@ -270,7 +273,11 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
 
     auto epilogue = [&](uint32_t jj, int64_t tt) {
       const uint32_t b = jj & 1;
+#if IQ_QJL_TCWAIT
+      mbar_wait_tc(&acc_full[b], (jj >> 1) & 1);        // completed by tcgen05.commit: no suspend hint
+#else
       mbar_wait(&acc_full[b], (jj >> 1) & 1);           // suspend-hint wait (compute warps)
+#endif
       tc_fence_after();
       const int row = 32 * quad + lane;
       const int64_t v = tt * TILE + row;
@@ -420,7 +427,11 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         // the previous tile's MMAs must have consumed the A tiles (the
         // stage-1 work above overlaps them)
 #if !IQ_QJL_NOWAIT_PROBE
+#if IQ_QJL_TCWAIT
+        if (u == 0) mbar_wait_tc(a_free, (j & 1) ^ 1);
+#else
         if (u == 0) mbar_wait(a_free, (j & 1) ^ 1);
+#endif
 #endif
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {

@@ -1,6 +1,7 @@
-"""GPU parity of the stage-2 residual sketch kernel (iq_quantize_qjl, the
-tcgen05 path) against the CPU oracle (oracle/qjl_oracle.py) on the same
-seeded inputs.  Tolerances (R20-R24, derived from the arithmetic):
+"""GPU parity of the stage-2 residual sketch (iq_quantize_qjl, the tcgen05
+path: one fused kernel at d in {64, 128}, quantizer + K-chunked sketch
+kernel at d in {256, 512}) against the CPU oracle (oracle/qjl_oracle.py) on
+the same seeded inputs.  Tolerances (R20-R24, derived from the arithmetic):
   * codes and norms bit-identical to iq_quantize (same kernel rule);
   * gamma = ||r|| within 2e-5 relative of the oracle's residual norm built
     from the GPU's own codes (x^ in fp32 vs fp64: ~1e-6 of ||r||);
@@ -83,14 +84,26 @@ def test_qjl_grid(variant, bits, d, dt):
     _check(X, d, bits, variant, dt)
 
 
+@pytest.mark.parametrize("dt", [iq.F16, iq.F32])
+@pytest.mark.parametrize("d", [256, 512])
+@pytest.mark.parametrize("bits", [1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [iq.FULL, iq.FAST, iq.PLANAR2D])
+def test_qjl_wide_grid(variant, bits, d, dt):
+    """The paper's wider heads: the quantizer + K-chunked sketch
+    kernel (S streamed from L2), 17 tiles with a ragged tail."""
+    X = iqsynth.unit_vectors(2048 + 37, d, 200 + bits + d, NP[dt])
+    _check(X, d, bits, variant, dt)
+
+
+@pytest.mark.parametrize("d", [128, 256, 512])
 @pytest.mark.parametrize("n", [1, 2, 127, 128, 129, 1000])
-def test_qjl_ragged(n):
-    X = iqsynth.unit_vectors(n, 128, 300 + n, np.float16)
-    _check(X, 128, 3, iq.FULL, iq.F16)
+def test_qjl_ragged(n, d):
+    X = iqsynth.unit_vectors(n, d, 300 + n, np.float16)
+    _check(X, d, 3, iq.FULL, iq.F16)
 
 
-def test_qjl_special_rows():
-    d = 128
+@pytest.mark.parametrize("d", [128, 512])
+def test_qjl_special_rows(d):
     rng = np.random.default_rng(4)
     X = iqsynth.unit_vectors(512, d, 55, np.float32)
     X[0] = 0.0                              # zero row: gamma = 0, all bits +1
@@ -106,11 +119,12 @@ def test_qjl_special_rows():
     assert float(rn[0]) == 0.0 and bool((qjl[0] == 0xFF).all())
 
 
-def test_qjl_large_batch_sample():
-    """2^20 rows (the cfg2 batch) in one launch; a 16384-row sample is
+@pytest.mark.parametrize("d", [128, 256, 512])
+def test_qjl_large_batch_sample(d):
+    """2^20 rows (the cfg2 batch) in one call; a 16384-row sample is
     checked against the oracle, and the mean of gamma^2 against the closed
     form d * E(z - Q(z))^2 of Appendix A.2."""
-    d, bits, n = 128, 3, 1 << 20
+    bits, n = 3, 1 << 20
     p = iq.iq_make_params_qjl(d, bits, iq.FULL, SEED, device=0)
     x = iqsynth.device_unit_vectors(n, d, 4321, torch.float16, "cuda")
     codes, norms, qjl, rn = iq.iq_quantize_qjl(p, x)
@@ -129,4 +143,4 @@ def test_qjl_errors():
     with pytest.raises(iq.IQError):
         iq.iq_quantize_qjl(p, x)                       # no sketch in this handle
     with pytest.raises(iq.IQError):
-        iq.iq_make_params_qjl(256, 3, iq.FULL, SEED, device=0)   # kernel supports d <= 128
+        iq.iq_make_params_qjl(32, 3, iq.FULL, SEED, device=0)    # GPU sketch: d in {64, 128, 256, 512}

@@ -47,6 +47,10 @@ VARIANTS = {
     "pu2": ["-DIQ_PAIR_UNROLL=2"],          # two row pairs per loop iteration (operator fetch shared)
     "b3fma64": ["-DIQ_B3_ALU=0", "-DIQ_STAGE_KB=64"],
     "b3fmapu2": ["-DIQ_B3_ALU=0", "-DIQ_PAIR_UNROLL=2"],
+    "opsreg12": ["-DIQ_OPS_SMEM=0", "-DIQ_NWC_NARROW=12"],   # operators in registers, 12 compute warps
+    "qjltc": ["-DIQ_QJL_TCWAIT=1"],         # stage-2 compute-warp waits without a suspend hint
+    "fhadd": ["-DIQ_FHADD=1"],              # fp16 -> fp32 by FHADD (full-rate) instead of HADD2.F32
+    "fhaddb3fma": ["-DIQ_FHADD=1", "-DIQ_B3_ALU=0"],
 }
 
 
