@@ -32,6 +32,9 @@ struct QGeo {
 #ifndef IQ_QJL_NOWAIT_PROBE
 #define IQ_QJL_NOWAIT_PROBE 0   // timing probe only: compute warps do not wait for the A tile (racy)
 #endif
+#ifndef IQ_QJL_MASKSPLIT
+#define IQ_QJL_MASKSPLIT 1   // fp16 hi by mantissa truncation (LOP3) instead of RN + convert back
+#endif
 #ifndef IQ_QJL_TCWAIT
 #define IQ_QJL_TCWAIT 0   // compute-warp waits on tcgen05.commit barriers without a suspend hint
 #endif
@@ -116,9 +119,11 @@ __device__ __forceinline__ uint32_t tmem_sign_word32(uint32_t taddr) {
         "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  // funnel the sign bits in, one SHF per bit: acc = (acc << 1) | (v_j >> 31)
+  // from j = 31 down, so bit j of acc is the sign of column j
   uint32_t neg = 0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) neg |= (v[j] >> 31) << j;
+  for (int j = 31; j >= 0; --j) neg = __funnelshift_l(v[j], neg, 1);
   return ~neg;
 }
 __device__ __forceinline__ uint32_t tmem_sign_word16(uint32_t taddr) {
@@ -132,7 +137,7 @@ __device__ __forceinline__ uint32_t tmem_sign_word16(uint32_t taddr) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   uint32_t neg = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) neg |= (v[j] >> 31) << j;
+  for (int j = 15; j >= 0; --j) neg = __funnelshift_l(v[j], neg, 1);
   return ~neg & 0xFFFFu;
 }
 
@@ -143,11 +148,20 @@ __device__ __forceinline__ void store_residual(uint8_t* a_hi, uint8_t* a_lo, uin
   uint32_t h[EPC / 2], l[EPC / 2];
 #pragma unroll
   for (int e = 0; e < EPC; e += 2) {
+#if IQ_QJL_MASKSPLIT
+    // hi = r truncated to 11 significant bits (exact in fp16 for |r| >=
+    // 2^-14), lo = r - hi exact in fp32 then rounded: r to ~2^-21 relative
+    const float h0 = __uint_as_float(__float_as_uint(rs[e]) & 0xFFFFE000u);
+    const float h1 = __uint_as_float(__float_as_uint(rs[e + 1]) & 0xFFFFE000u);
+    h[e / 2] = pack2<__half>(h0, h1);
+    l[e / 2] = pack2<__half>(rs[e] - h0, rs[e + 1] - h1);
+#else
     const __half2 hh = __floats2half2_rn(rs[e], rs[e + 1]);
     const float2 hf = __half22float2(hh);
     const __half2 ll = __floats2half2_rn(rs[e] - hf.x, rs[e + 1] - hf.y);
     h[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
     l[e / 2] = *reinterpret_cast<const uint32_t*>(&ll);
+#endif
   }
   if constexpr (EPC == 8) {
     *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(h[0], h[1], h[2], h[3]);

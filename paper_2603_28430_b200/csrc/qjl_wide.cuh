@@ -68,6 +68,13 @@ struct WGeo {
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
+// TMA prefetch of a contiguous global range into L2 (no shared memory, no
+// completion tracking): the next tile's rows are on chip by the time the
+// compute threads' loads ask for them
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -338,10 +345,21 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     ++c;
   };
 
+  // L2 prefetch of the rows of tile t (x, codes, norms), one tile ahead
+  auto prefetch_tile = [&](int64_t t) {
+    if (t < ntiles && threadIdx.x == 0) {
+      const int64_t v0 = t * TILE, nv = (n - v0) < TILE ? (n - v0) : TILE;
+      prefetch_l2(x + v0 * D, (uint32_t)(nv * D * sizeof(T)));
+      prefetch_l2(codes + v0 * RB, (uint32_t)((nv * RB + 15) & ~15));
+      prefetch_l2(norms + v0, (uint32_t)((nv * 4 + 15) & ~15));
+    }
+  };
+  prefetch_tile(blockIdx.x);
   Raw f0, f1;
   fetch(blockIdx.x, 0, f0);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
     const int64_t ra = t * TILE + rp, rb = ra + 64;
+    prefetch_tile(t + gridDim.x);
 #pragma unroll 1
     for (int k = 0; k < NKC; k += 2) {               // ping-pong: the next item loads while this one computes
       fetch(t, k + 1, f1);

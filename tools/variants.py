@@ -48,7 +48,11 @@ VARIANTS = {
     "b3fma64": ["-DIQ_B3_ALU=0", "-DIQ_STAGE_KB=64"],
     "b3fmapu2": ["-DIQ_B3_ALU=0", "-DIQ_PAIR_UNROLL=2"],
     "opsreg12": ["-DIQ_OPS_SMEM=0", "-DIQ_NWC_NARROW=12"],   # operators in registers, 12 compute warps
-    "qjltc": ["-DIQ_QJL_TCWAIT=1"],         # stage-2 compute-warp waits without a suspend hint
+    "tpl8": ["-DIQ_TPL_K3=8"],              # fused kernel: 8 coordinates per lane (operators in registers)
+    "tpl8w12": ["-DIQ_TPL_K3=8", "-DIQ_NWC_WIDE=12"],
+    "tpl8w20": ["-DIQ_TPL_K3=8", "-DIQ_NWC_WIDE=20"],
+    "qjltc": ["-DIQ_QJL_TCWAIT=1"],
+    "qjlrn": ["-DIQ_QJL_MASKSPLIT=0"],     # stage-2 hi/lo split by RN + convert back (round-1 form)         # stage-2 compute-warp waits without a suspend hint
     "fhadd": ["-DIQ_FHADD=1"],              # fp16 -> fp32 by FHADD (full-rate) instead of HADD2.F32
     "fhaddb3fma": ["-DIQ_FHADD=1", "-DIQ_B3_ALU=0"],
 }
