@@ -211,6 +211,17 @@ def read_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def read_tensor_peak() -> float:
+    """Dense fp16/bf16 tensor peak (TFLOP/s): MEASURED_PEAKS.json's sustained
+    cuBLAS bf16 figure (fp16 has the same rate), else the nominal 2250."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d.get("bf16_tflops_sustained") or d["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
 def read_traffic(key: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -599,6 +610,47 @@ def kernel_entries(torch, iq, iqsynth, a, p, xs, ys, n, vid, dev, stream, peak, 
                                     "bytes_per_launch": b, "keys_per_s": H * nk / (t / 1e3),
                                     "shape": f"{H} heads x {nk} keys, 4 queries per head, stage 1"}
         del qh, sc
+    # quantize-on-append (NEXT row 2): one decode step of a [32 layers x 8 KV
+    # heads] cache (256 slots, one new token each, per-(layer, head) parameter
+    # sets), and 64 concurrent sequences (16384 slots) for the bandwidth view
+    ps = iq.iq_make_params_sets(a.d, a.bits, vid, iqsynth.PARAMS_SEED, 256, 1, device=dev.index)
+    for slots, what in ((256, "one decode step, 32 layers x 8 KV heads"),
+                        (16384, "64 sequences x 32 layers x 8 KV heads")):
+        if slots > n:
+            continue
+        cap = 8
+        xa = xs[0][:slots]
+        ca = torch.empty((slots, cap, ps.code_bytes), dtype=torch.uint8, device=dev)
+        na = torch.empty((slots, cap), dtype=torch.float32, device=dev)
+        t = time_launches(torch, lambda i: iq.iq_append_kv(ps, xa, ca, na, position=i % cap, stream=stream),
+                          max(20, a.steps), 5, stream)
+        b = slots * bytes_per_vector("quantize", a.d, a.bits, s)
+        kern[f"append_kv_{slots}"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                                      "keys_per_s": slots / (t / 1e3), "bytes_per_launch": b, "shape": what}
+        del ca, na
+    # stage 2 at the paper's widths (NEXT row 1): 2^20 rows, b = 3, fp16;
+    # d in {256, 512} is the quantizer + the K-chunked sketch kernel.  The
+    # tensor roofline counts 4 d m flop per row (hi + lo passes, m = d).
+    if a.dtype == "f16" and a.bits == 3 and a.variant == "full" and n >= (1 << 20):
+        st2 = {}
+        for dd in (128, 256, 512):
+            pq = iq.iq_make_params_qjl(dd, 3, vid, iqsynth.PARAMS_SEED, device=dev.index)
+            nn = 1 << 20
+            xq = iqsynth.device_unit_vectors(nn, dd, 77, torch.float16, dev)
+            cq_ = torch.empty((nn, pq.code_bytes), dtype=torch.uint8, device=dev)
+            nq_ = torch.empty(nn, dtype=torch.float32, device=dev)
+            qj = torch.empty((nn, dd // 8), dtype=torch.uint8, device=dev)
+            rn = torch.empty(nn, dtype=torch.float32, device=dev)
+            t = time_launches(torch, lambda i: iq.iq_quantize_qjl(pq, xq, cq_, nq_, qj, rn, stream=stream),
+                              10, 3, stream)
+            b = nn * bytes_per_vector("quantize_qjl", dd, 3, 2)
+            fl = nn * 4 * dd * dd
+            st2[f"d{dd}"] = {"us": 1e3 * t, "GB/s": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peak,
+                             "tensor_tflops": fl / (t / 1e3) / 1e12,
+                             "tensor_frac": fl / (t / 1e3) / 1e12 / read_tensor_peak(),
+                             "launches": 1 if dd <= 128 else 2}
+            del xq, cq_, nq_, qj, rn
+        kern["quantize_qjl_by_width"] = st2
     # context: a plain device-to-device copy of the same bytes (torch's copy
     # kernel, not on our path) timed the same way on this box
     if not inplace:
