@@ -86,6 +86,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernels", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the in-run ncu DRAM-traffic measurement")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
@@ -220,6 +221,50 @@ def read_tensor_peak() -> float:
         return float(d.get("bf16_tflops_sustained") or d["bf16_tflops"])
     except Exception:
         return 2250.0
+
+
+_UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def parse_ncu_dram(text: str) -> dict:
+    """{metric: bytes} for dram__bytes_{read,write}.sum from `ncu --csv` output
+    (one launch; non-CSV lines such as the ==PROF== banner are skipped)."""
+    import csv
+    import io
+    lines = [ln for ln in text.splitlines() if ln.startswith('"')]
+    vals = {}
+    for row in csv.DictReader(io.StringIO("\n".join(lines))):
+        name = row.get("Metric Name")
+        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v = float(row.get("Metric Value", "nan").replace(",", ""))
+            vals[name] = v * _UNIT.get(row.get("Metric Unit", "byte"), 1.0)
+    return vals
+
+
+def measure_traffic(a, rows: int, timeout_s: float = 240.0):
+    """DRAM bytes (read + write) per launch of the bench's kernel at the bench's
+    size, measured in this run: ncu (two counters, one launch after a warm-up
+    launch) around tools/launch_kernels.py in a child process.  The child's
+    timings are never used.  Returns (bytes or None, note)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "-k", "regex:k_encode", "--launch-skip", "1", "--launch-count", "1", "--csv", "--print-units", "base",
+           sys.executable, os.path.join(ROOT, "tools", "launch_kernels.py"), "--kernel", "roundtrip",
+           "--variant", a.variant, "--d", str(a.d), "--bits", str(a.bits), "--dtype", a.dtype,
+           "--n", str(rows), "--reps", "2"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu failed: {type(e).__name__}"
+    vals = parse_ncu_dram(r.stdout)
+    if len(vals) != 2:
+        return None, f"ncu produced no DRAM counters (rc={r.returncode})"
+    return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"], (
+        "measured in this run: ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch of this kernel "
+        "at this size (child process, cold L2)")
 
 
 def read_traffic(key: str):
@@ -496,10 +541,16 @@ def main():
     bpl = rows * bytes_per_vector("roundtrip", a.d, a.bits, s)
     achieved = bpl / (ms / a.steps / 1e3) / 1e9
     key = f"roundtrip_{a.variant}_d{a.d}_b{a.bits}_{a.dtype}_n{rows}"
+    traffic, tsrc = (None, "not measured (--no-traffic / profile mode)")
+    if rank == 0 and world == 1 and not (a.profile or a.no_traffic):
+        if 2 * rows * a.d * s <= torch.cuda.mem_get_info(dev)[0] // 2:   # the child needs its own x and y
+            traffic, tsrc = measure_traffic(a, rows)
+        else:
+            tsrc = "not measured in this run (the ncu child would not fit next to the bench's buffers)"
+    if traffic is None and read_traffic(key) is not None:
+        traffic, tsrc = read_traffic(key), tsrc + "; value from profiles/traffic.json (an earlier ncu capture)"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": read_traffic(key),
-                "traffic_source": "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum of one "
-                                  "ncu --set full capture of this kernel at this size, per launch)",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
                 "kernel": f"k_encode<{a.dtype},{a.d},{a.bits},{a.variant},MODE 1 (fused, no codes)>",
                 "algorithmic_bytes_per_launch": bpl, "peak_source": peak_src,
                 "timing": "sustained: 0.4 s untimed settle under load, then the K timed steps (CUDA events)"}

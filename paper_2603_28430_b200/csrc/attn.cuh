@@ -115,9 +115,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   float* qs = reinterpret_cast<float*>(smem + A::QS_OFF);   // [2][NQ]: 1/sigma_j, 8/sigma_j
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + A::BAR_OFF);
   uint64_t* empty = full + NST;
-  uint64_t* a_full = empty + NST;      // [2] decoders -> MMA
-  uint64_t* a_free = a_full + 2;       // [2] MMA -> decoders (A buffer consumed)
-  uint64_t* acc_full = a_free + 2;     // [NACC] MMA -> epilogue
+  uint64_t* a_full = empty + NST;      // [4] decoders -> MMA
+  uint64_t* a_free = a_full + 4;       // [4] MMA -> decoders (A buffer consumed)
+  uint64_t* acc_full = a_free + 4;     // [NACC] MMA -> epilogue
   uint64_t* acc_empty = acc_full + A::NACC;   // [NACC] epilogue -> MMA, decoders (accumulator, side table free)
   uint64_t* side_full = acc_empty + A::NACC;  // [NACC] decoders -> epilogue: side table written
   uint64_t* s_bar = side_full + A::NACC;      // S image staged (per head change)
@@ -128,7 +128,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWD); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1); }
+    for (int b = 0; b < 4; ++b) { mbar_init(&a_full[b], NWD); mbar_init(&a_free[b], 1); }
     for (int c = 0; c < A::NACC; ++c) {
       mbar_init(&acc_full[c], 1); mbar_init(&acc_empty[c], A::NWE);
       mbar_init(&side_full[c], (2 * TILE) / 32);   // the warps that write rho / gamma / scales
@@ -153,6 +153,11 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
   const int64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t_begin = blockIdx.x * per_cta;
   const int64_t t_end = (t_begin + per_cta) < ntiles ? (t_begin + per_cta) : ntiles;
+  // A operand buffers in flight: without the stage-2 term its part of each
+  // double buffer is free, so stage 1 runs four single-part buffers deep
+  // (more decoded tiles queued ahead of the tensor pipe's completion latency)
+  const uint32_t nab = (A::ST2OK && !st2) ? 2u * NPART : 2u;
+  const uint32_t a_stride = (A::ST2OK && !st2) ? (uint32_t)A::A_BYTES : (uint32_t)(NPART * A::A_BYTES);
 
   if (warp == A::W_PROD) {  // ---------------------------------------- TMA producer
     if (lane == 0) {
@@ -192,12 +197,12 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         mbar_wait_tc(&acc_empty[c], (u & 1) ^ 1);
 #pragma unroll 1
         for (int kc = 0; kc < KC; ++kc, ++jj) {
-          const uint32_t b = jj & 1;
-          mbar_wait_tc(&a_full[b], (jj >> 1) & 1);
+          const uint32_t b = jj % nab;
+          mbar_wait_tc(&a_full[b], (jj / nab) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int part = 0; part < (st2 ? 2 : 1); ++part) {
-            const uint32_t ta = ab + (NPART * b + part) * A::A_BYTES, tb = bb + part * A::B_BYTES;
+            const uint32_t ta = ab + b * a_stride + part * A::A_BYTES, tb = bb + part * A::B_BYTES;
             const uint32_t td = tmem + (2 * c + part) * NQ;
 #pragma unroll
             for (int s = 0; s < KCH / 16; ++s)
@@ -385,7 +390,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       if (h != hcur) {
         // drain: the last MMA issued (chunk jj - 1) completes after every
         // earlier one, so the B tiles and both A buffers are free
-        if (jj > 0) mbar_wait_tc(&a_free[(jj - 1) & 1], ((jj - 1) >> 1) & 1);
+        if (jj > 0) mbar_wait_tc(&a_free[(jj - 1) % nab], ((jj - 1) / nab) & 1);
         load_queries(h);
         hcur = h;
         if (threadIdx.x < 2 * NQ) qs_mine = qs[threadIdx.x];
@@ -466,9 +471,9 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       }
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc, ++jj) {
-        const uint32_t b = jj & 1;
-        mbar_wait_tc(&a_free[b], ((jj >> 1) & 1) ^ 1);      // A[b] consumed by the MMAs of chunk jj - 2
-        uint8_t* a1 = a_base + (NPART * b) * A::A_BYTES;
+        const uint32_t b = jj % nab;
+        mbar_wait_tc(&a_free[b], ((jj / nab) & 1) ^ 1);     // A[b] consumed by the MMAs of chunk jj - nab
+        uint8_t* a1 = a_base + b * a_stride;
         uint8_t* a2 = a1 + A::A_BYTES;
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) {

@@ -58,3 +58,22 @@ def test_clocks_not_rejected(line):
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     assert not bad.intersection(c["reasons"])
     assert c["sm_mhz"] > 0.7 * c["sm_max_mhz"]
+
+
+def test_ncu_dram_csv_parsing():
+    """bench.py's in-run traffic measurement reads ncu's --csv metric rows
+    (base units, or auto-scaled units) and ignores the banner lines."""
+    import bench
+    text = "\n".join([
+        "==PROF== Connected to process 1 (python)",
+        '"ID","Process ID","Process Name","Host Name","Kernel Name","Context","Stream","Block Size","Grid Size",'
+        '"Device","CC","Section Name","Metric Name","Metric Unit","Metric Value"',
+        '"0","1","python","h","void iq::k_encode<__half, 128, 3, 0, 1, 0>(...)","1","7","(544, 1, 1)",'
+        '"(148, 1, 1)","0","10.0","Command line profiler metrics","dram__bytes_read.sum","byte","268,453,888"',
+        '"0","1","python","h","void iq::k_encode<__half, 128, 3, 0, 1, 0>(...)","1","7","(544, 1, 1)",'
+        '"(148, 1, 1)","0","10.0","Command line profiler metrics","dram__bytes_write.sum","Mbyte","217.58"',
+        "==PROF== Disconnected from process 1",
+    ])
+    v = bench.parse_ncu_dram(text)
+    assert v["dram__bytes_read.sum"] == 268453888.0
+    assert abs(v["dram__bytes_write.sum"] - 217.58e6) < 1.0

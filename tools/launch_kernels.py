@@ -30,7 +30,8 @@ def main():
     y = torch.empty_like(x)
     codes = torch.empty((a.n, p.code_bytes), dtype=torch.uint8, device="cuda")
     norms = torch.empty(a.n, dtype=torch.float32, device="cuda")
-    iq.iq_quantize(p, x, codes, norms)
+    if a.kernel != "roundtrip":           # (the fused kernel needs no codes: keep its launch the only one)
+        iq.iq_quantize(p, x, codes, norms)
     if a.kernel in ("quantize_qjl", "attention", "all"):
         pq = iq.iq_make_params_qjl(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
         qj = torch.empty((a.n, a.d // 8), dtype=torch.uint8, device="cuda")
