@@ -274,6 +274,25 @@ __device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t par
       : "memory");
   return ok != 0;
 }
+// try_wait with a short suspend-time hint (~256 ns): for barriers completed
+// by tcgen05.commit that a whole warp waits on -- parks the lanes instead of
+// spinning (shared-memory traffic next to the tensor pipe's operand reads)
+// while bounding the oversleep
+__device__ __forceinline__ bool mbar_try_wait_short(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 256;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_short(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_short(bar, parity)) {
+  }
+}
 #ifndef IQ_TC_SPIN
 #define IQ_TC_SPIN 1
 #endif

@@ -26,7 +26,7 @@
 //                (a shared-memory arrival counter), so no warp is parked
 //                on the tensor pipe: z (+)= A_hi S_k^T + A_lo S_k^T, M = 128
 //                rows, N = m (one or two N = 256 instructions per K-step),
-//                fp32 in TMEM; the same thread tops up the S ring;
+//                fp32 in TMEM; the same thread refills the S ring;
 //   epilogue   : tcgen05.ld, sign bits [z >= 0] packed LSB-first (R22).
 // The residual arithmetic is the fused d <= 128 kernel's direct form
 // (qjl.cuh, fp32 rows), so the two agree on the readings.
@@ -40,16 +40,18 @@ struct WGeo {
   static constexpr int PW = (VAR == IQ_VARIANT_PLANAR2D) ? 2 : 4;   // block width
   static constexpr int M = D;                    // sketch rows (R20)
   static constexpr int TILE = 128;               // rows per tile = UMMA M
+  static constexpr int NPC = M / 256;            // N = 256 MMA pieces per K-step
+  static constexpr int NWC = 16;                 // compute warps: (row pair, piece) = thread; no dedicated MMA warp
   static constexpr int KC = 64;                  // coordinates per K-chunk (one 128-byte swizzle atom)
   static constexpr int NKC = D / KC;
-  static constexpr int NPC = M / 256;            // N = 256 MMA pieces per K-step
-  static constexpr int NWC = 16;                 // warps: (row pair, piece) = thread; no dedicated MMA warp
-  static constexpr int CTA_THREADS = 32 * NWC;   // 4 warps per sub-partition: 128 registers per thread
-  static constexpr int RB = D * BITS / 8;        // code bytes per row
   static constexpr int B_STAGE = M * 128;        // one K-chunk of S: m rows x 64 fp16
-  // d = 256: all of S (128 KB) stays resident (loaded once per CTA);
-  // d = 512: S (512 KB) streams from L2 through a two-stage ring
+  // d = 256: all of S (128 KB) stays resident (loaded once per CTA), 16
+  // warps (4 per sub-partition: 128 registers); d = 512: S (512 KB) streams
+  // from L2 through a two-stage ring refilled by a dedicated TMA warp (the
+  // refill must not wait for a compute warp to reach a polling point)
   static constexpr bool RES = NKC * B_STAGE <= 128 * 1024;
+  static constexpr int CTA_THREADS = 32 * (NWC + (RES ? 0 : 1));
+  static constexpr int RB = D * BITS / 8;        // code bytes per row
   static constexpr int NB = RES ? NKC : 2;        // S stages
   static constexpr int A_TILE = TILE * 128;      // one fp16 operand chunk (hi or lo): 16 KB
   static constexpr int NA = 2;                   // A ring depth (hi + lo per stage)
@@ -103,13 +105,16 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
   uint64_t* acc_empty = acc_full + NACC; // epilogue read the accumulator (NWC arrivals)
   uint32_t* arrivals = reinterpret_cast<uint32_t*>(acc_empty + NACC);   // [NA] warps done with the stage
   uint32_t* tmem_slot = arrivals + NA;
-  uint32_t* issued_slot = tmem_slot + 1; // S chunk loads issued (streaming; one writer at a time)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + TILE - 1) / TILE;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const uint32_t total = (uint32_t)(my_tiles * NKC);   // K-chunks this CTA produces
   const uint64_t pol = policy_evict_last();            // S is re-read by every CTA: keep it in L2
+  // streamed S: CTA i walks the K-chunks starting at chunk i mod NKC, so at
+  // any moment the 148 CTAs read different parts of S (the same 64 KB from
+  // every SM at once is an L2 hot spot: measured 1.5-2.6 ms, unstable)
+  const int rot = W::RES ? 0 : (int)(blockIdx.x % NKC);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int s = 0; s < NA; ++s) { mbar_init(&a_empty[s], 1); arrivals[s] = 0; }
@@ -119,9 +124,8 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     const uint32_t first = W::RES ? (uint32_t)NB : (total < (uint32_t)NB ? total : (uint32_t)NB);
     for (uint32_t k = 0; k < first; ++k) {
       mbar_arrive_expect_tx(&b_full[k], W::B_STAGE);
-      bulk_g2s(b_ring + k * W::B_STAGE, s_img + (size_t)(k % NKC) * W::B_STAGE, W::B_STAGE, &b_full[k], pol);
+      bulk_g2s(b_ring + k * W::B_STAGE, s_img + (size_t)((k + rot) % NKC) * W::B_STAGE, W::B_STAGE, &b_full[k], pol);
     }
-    *issued_slot = first;
   }
   // every block operator, as float4 q of block b of piece p at
   // (u * NQ + q) * (D / 8) + p with b = p * BPP + u: the 8 pieces of a chunk
@@ -141,28 +145,9 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
 
   // D[128 x 256] (+)= A[128 x 16] * B[256 x 16]^T per instruction: fp16, fp32 accumulate
   constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
-  // streaming: issue S loads up to NB chunks ahead of chunk c; a stage is
-  // reused once the MMAs that read it completed (b_empty), polled without
-  // blocking unless `need` (the chunk about to be multiplied) is not loaded
-  auto top_up = [&](uint32_t c, bool block) {
-    if constexpr (!W::RES) {
-      uint32_t issued = *reinterpret_cast<volatile uint32_t*>(issued_slot);
-      while (issued < total && issued < c + NB) {
-        const int st = issued % NB;
-        const uint32_t par = ((issued / NB) & 1) ^ 1;
-        if (block && issued <= c) mbar_wait_tc(&b_empty[st], par);
-        else if (!mbar_try_wait_nohint(&b_empty[st], par)) break;
-        mbar_arrive_expect_tx(&b_full[st], W::B_STAGE);
-        bulk_g2s(b_ring + st * W::B_STAGE, s_img + (size_t)(issued % NKC) * W::B_STAGE, W::B_STAGE, &b_full[st], pol);
-        ++issued;
-      }
-      *reinterpret_cast<volatile uint32_t*>(issued_slot) = issued;
-    }
-  };
   // the MMAs of chunk c (K-chunk k of accumulator b), by the last warp to finish it
   auto issue = [&](uint32_t c, int k, uint32_t b, bool last_of_tile) {
     const int sa = c % NA, sb = W::RES ? k : (int)(c % NB);
-    top_up(c, true);
     mbar_wait_tc(&b_full[sb], W::RES ? 0u : (c / NB) & 1);
     tc_fence_after();
     const uint32_t ah = smem_u32(a_ring + 2 * sa * W::A_TILE), al = ah + W::A_TILE;
@@ -178,9 +163,22 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     umma_commit(&a_empty[sa]);
     if constexpr (!W::RES) umma_commit(&b_empty[sb]);
     if (last_of_tile) umma_commit(&acc_full[b]);
-    top_up(c + 1, false);
   };
 
+  if constexpr (!W::RES) {
+    if (warp == NWC) {   // ------------------------------ streamed S: the TMA refill warp
+      if (lane == 0) {
+        for (uint32_t u = NB; u < total; ++u) {   // chunk u reuses the stage of chunk u - NB
+          const int st = u % NB;
+          mbar_wait_tc(&b_empty[st], ((u / NB) & 1) ^ 1);   // completed by tcgen05.commit
+          mbar_arrive_expect_tx(&b_full[st], W::B_STAGE);
+          bulk_g2s(b_ring + st * W::B_STAGE, s_img + (size_t)((u + rot) % NKC) * W::B_STAGE, W::B_STAGE,
+                   &b_full[st], pol);
+        }
+      }
+    }
+  }
+  if (warp < NWC) {    // ------------------------------------------------ compute warps
   const int tid = threadIdx.x;
   const int pc = tid & 7;                 // 8-coordinate piece of the chunk
   const int rp = tid >> 3;                // row pair: tile rows rp and rp + 64
@@ -225,7 +223,7 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     if (t >= ntiles) return;
     const int64_t ra = t * TILE + rp, rb = ra + 64;
     const int64_t la = ra < n ? ra : n - 1, lb = rb < n ? rb : n - 1;   // clamped for the ragged tail
-    const int q = k * 8 + pc;                                           // coordinates 8 q .. 8 q + 7
+    const int q = ((k + rot) % NKC) * 8 + pc;                           // coordinates 8 q .. 8 q + 7
 #pragma unroll
     for (int i = 0; i < W::XV; ++i) {
       f.xa[i] = __ldg(reinterpret_cast<const uint4*>(x + la * D + 8 * q) + i);
@@ -271,15 +269,23 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
       sr = f2(256.0f * rcp_approx(fmaxf(cur.rho_a, 1e-12f)), 256.0f * rcp_approx(fmaxf(cur.rho_b, 1e-12f)));
       g2 = bc(0.0f);
     }
-    const int q = k * 8 + pc;
+    const int q = ((k + rot) % NKC) * 8 + pc;     // this step's K-chunk (rotated per CTA when S streams)
     const uint32_t wa = BITS == 3 ? __funnelshift_r(cur.ca0, cur.ca1, cshift) : cur.ca0 >> cshift;
     const uint32_t wb = BITS == 3 ? __funnelshift_r(cur.cb0, cur.cb1, cshift) : cur.cb0 >> cshift;
     float va[8], vb[8];
     unpack8(cur.xa, va);
     unpack8(cur.xb, vb);
     const int sa = c % NA;
-    if (lane == 0) mbar_wait_tc(&a_empty[sa], ((c / NA) & 1) ^ 1);   // the MMAs of the stage's last use are done
-    __syncwarp();
+    // the MMAs of the stage's last use are done.  Resident S (d = 256):
+    // every lane waits, parked with a short suspend hint (the warp stays
+    // converged for its shuffles: 0.74 -> 0.58 ms); streamed S (d = 512):
+    // one lane waits (measured 15 % faster there)
+    if constexpr (W::RES) {
+      mbar_wait_short(&a_empty[sa], ((c / NA) & 1) ^ 1);
+    } else {
+      if (lane == 0) mbar_wait_tc(&a_empty[sa], ((c / NA) & 1) ^ 1);
+      __syncwarp();
+    }
     uint8_t* ah = a_ring + 2 * sa * W::A_TILE;
     uint8_t* al = ah + W::A_TILE;
     // the piece as two quads of coordinates (one 4-D block or two 2-D
@@ -385,6 +391,7 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     tprev = t;
   }
   if (tprev >= 0) epilogue(j - 1, tprev);
+  }  // compute warps
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
