@@ -66,6 +66,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_B3_ALU
 #define IQ_B3_ALU 1          // b = 3 fused value chain: FSETP + predicated FADD (else FSET + FFMA2)
 #endif
+#ifndef IQ_GRID_PAIR
+#define IQ_GRID_PAIR 0       // b = 4 grid decision with the two rows' FFMAs packed as FFMA2 (measured slower)
+#endif
 #ifndef IQ_FHADD
 #define IQ_FHADD 0           // fp16 -> fp32 with the mixed-precision FHADD (else HADD2.F32)
 #endif
@@ -659,6 +662,25 @@ __device__ __forceinline__ uint32_t grid_index(float y, float sc, float gtab, ui
   const float dlt = __fmaf_rn(-fabsf(y), sc, __shfl_sync(kFull, gtab, (int)t));
   return t + (__float_as_uint(dlt) >> 31);
 }
+// The same for a coordinate pair (row A in .x, row B in .y, per-row scales):
+// the two FFMAs run as packed FFMA2 (.RM and RN), bit-identical lane by
+// lane to grid_index; one FMA-pipe instruction per pair instead of two.
+__device__ __forceinline__ void grid_index2(float2 y, float2 sc, float gtab, uint32_t gclamp, uint32_t& ia,
+                                            uint32_t& ib) {
+  const float2 ay = f2(fabsf(y.x), fabsf(y.y));
+  float2 u;
+  asm("{.reg .b64 a, b, c, d;\n"
+      "mov.b64 a, {%2, %3}; mov.b64 b, {%4, %5}; mov.b64 c, {%6, %6};\n"
+      "fma.rm.f32x2 d, a, b, c;\n"
+      "mov.b64 {%0, %1}, d;}"
+      : "=f"(u.x), "=f"(u.y)
+      : "f"(ay.x), "f"(ay.y), "f"(sc.x), "f"(sc.y), "f"(8388608.0f));
+  const uint32_t ta = min(__float_as_uint(u.x), gclamp), tb = min(__float_as_uint(u.y), gclamp);
+  const float2 thr = f2(__shfl_sync(kFull, gtab, (int)ta), __shfl_sync(kFull, gtab, (int)tb));
+  const float2 dlt = fma2(f2(-ay.x, -ay.y), sc, thr);
+  ia = ta + (__float_as_uint(dlt.x) >> 31);
+  ib = tb + (__float_as_uint(dlt.y) >> 31);
+}
 // signed code of a grid index: (m | h) for ybar >= 0, h - 1 - m = (m | h) ^ (2h - 1) below
 template <int BITS>
 __device__ __forceinline__ uint32_t grid_code(uint32_t idx, float y, uint32_t gcode) {
@@ -842,8 +864,13 @@ __device__ __forceinline__ void encode_pair(
       rot_fwd<PW>(Mb, v + b * PW, yb);               // T(x)  (Alg.1 l.5/9/13)
 #pragma unroll
       for (int j = 0; j < PW; ++j) {
-        const uint32_t ia = grid_index(yb[j].x, sc.x, gtab, cb.gclamp);
-        const uint32_t ib = grid_index(yb[j].y, sc.y, gtab, cb.gclamp);
+        uint32_t ia, ib;
+#if IQ_GRID_PAIR
+        grid_index2(yb[j], sc, gtab, cb.gclamp, ia, ib);
+#else
+        ia = grid_index(yb[j].x, sc.x, gtab, cb.gclamp);
+        ib = grid_index(yb[j].y, sc.y, gtab, cb.gclamp);
+#endif
         if constexpr (emit) {
           const int e = (b * PW + j) % EPC, c = (b * PW + j) / EPC;
           cwa[c] |= grid_code<BITS>(ia, yb[j].x, gcode) << (e * BITS);

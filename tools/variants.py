@@ -54,6 +54,7 @@ VARIANTS = {
     "qjltc": ["-DIQ_QJL_TCWAIT=1"],
     "qjlrn": ["-DIQ_QJL_MASKSPLIT=0"],
     "qjlhint": ["-DIQ_QJL_MMA_HINT=1"],     # stage-2 MMA warp: parked waits     # stage-2 hi/lo split by RN + convert back (round-1 form)         # stage-2 compute-warp waits without a suspend hint
+    "gridpair": ["-DIQ_GRID_PAIR=1"],       # b = 4 grid decision with the rows' FFMAs packed (FFMA2.RM / FFMA2)
     "fhadd": ["-DIQ_FHADD=1"],              # fp16 -> fp32 by FHADD (full-rate) instead of HADD2.F32
     "fhaddb3fma": ["-DIQ_FHADD=1", "-DIQ_B3_ALU=0"],
 }
