@@ -73,7 +73,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #define IQ_FHADD 0           // fp16 -> fp32 with the mixed-precision FHADD (else HADD2.F32)
 #endif
 #ifndef IQ_PAIR_UNROLL
-#define IQ_PAIR_UNROLL 1
+#define IQ_PAIR_UNROLL 2     // two row pairs per loop iteration (K1 1.5-2 % faster, K3 unchanged; measured)
 #endif
 constexpr int kPairUnroll = IQ_PAIR_UNROLL;    // row pairs interleaved per iteration
 constexpr int kThreads = 256;                  // statistics kernel CTAs

@@ -44,7 +44,7 @@ VARIANTS = {
     "qjl1mma": ["-DIQ_QJL_PASSES=1"],       # timing probe only: one MMA pass (inexact sketch)
     "qjlnowait": ["-DIQ_QJL_NOWAIT_PROBE=1"],   # timing probe only: A tile reuse without the MMA wait (racy)
     "norotd": ["-DIQ_QJL_ROTD=0"],          # stage 2 residual in the input domain (2 passes)
-    "pu2": ["-DIQ_PAIR_UNROLL=2"],          # two row pairs per loop iteration (operator fetch shared)
+    "pu1": ["-DIQ_PAIR_UNROLL=1"],          # one row pair per loop iteration (round-1 form)
     "b3fma64": ["-DIQ_B3_ALU=0", "-DIQ_STAGE_KB=64"],
     "b3fmapu2": ["-DIQ_B3_ALU=0", "-DIQ_PAIR_UNROLL=2"],
     "opsreg12": ["-DIQ_OPS_SMEM=0", "-DIQ_NWC_NARROW=12"],   # operators in registers, 12 compute warps
@@ -54,6 +54,8 @@ VARIANTS = {
     "qjltc": ["-DIQ_QJL_TCWAIT=1"],
     "qjlrn": ["-DIQ_QJL_MASKSPLIT=0"],
     "qjlhint": ["-DIQ_QJL_MMA_HINT=1"],     # stage-2 MMA warp: parked waits     # stage-2 hi/lo split by RN + convert back (round-1 form)         # stage-2 compute-warp waits without a suspend hint
+    "pu2w8": ["-DIQ_PAIR_UNROLL=2", "-DIQ_NWC_WIDE=8"],     # two row pairs per iteration, 8 compute warps
+    "pu2w12": ["-DIQ_PAIR_UNROLL=2", "-DIQ_NWC_WIDE=12"],
     "gridpair": ["-DIQ_GRID_PAIR=1"],       # b = 4 grid decision with the rows' FFMAs packed (FFMA2.RM / FFMA2)
     "fhadd": ["-DIQ_FHADD=1"],              # fp16 -> fp32 by FHADD (full-rate) instead of HADD2.F32
     "fhaddb3fma": ["-DIQ_FHADD=1", "-DIQ_B3_ALU=0"],
