@@ -461,24 +461,41 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus and rank == 0:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    # IQ_BENCH_SHARED_GPU=1 (functional check of the N > 1 path on a one-GPU
+    # box): every rank on cuda:0, gloo for the statistics (NCCL refuses two
+    # ranks on one device).  The throughput is then one GPU's, shared.
+    shared = os.environ.get("IQ_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl = None
     if world > 1:
-        # NCCL's init lines (communicator size, transports, NVLS) on stderr, so
-        # the communicator is verifiable without mixing into the JSON line
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        dist.init_process_group("nccl", device_id=dev)
-        one = torch.ones(1, device=dev)
-        dist.all_reduce(one)                                   # communicator up: counts the ranks
-        nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
-                "allreduce_of_ones": int(one.item()), "version": ".".join(map(str, torch.cuda.nccl.version()))}
+        if shared:
+            dist.init_process_group("gloo")
+            one = torch.ones(1)
+            dist.all_reduce(one)
+            nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                    "allreduce_of_ones": int(one.item()), "shared_gpu": True}
+        else:
+            # NCCL's init lines (communicator size, transports, NVLS) on stderr,
+            # so the communicator is verifiable without mixing into the JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            dist.init_process_group("nccl", device_id=dev)
+            one = torch.ones(1, device=dev)
+            dist.all_reduce(one)                               # communicator up: counts the ranks
+            nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                    "allreduce_of_ones": int(one.item()), "version": ".".join(map(str, torch.cuda.nccl.version()))}
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if shared:
+                torch.cuda.synchronize()
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     from __graft_entry__ import load_builder
     _build = load_builder()
