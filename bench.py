@@ -77,7 +77,7 @@ def parse_args():
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--bits", type=int, default=3)
     ap.add_argument("--dtype", default="f16", choices=["f16", "f32"])
-    ap.add_argument("--n", type=int, default=1 << 20,
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=1 << 20,
                     help="vectors per GPU (weak scaling) or in the global batch (strong scaling)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--preset", choices=sorted(PRESETS), default=None,
