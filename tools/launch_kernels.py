@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--dtype", default="f16")
     ap.add_argument("--n", type=int, default=1 << 20)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--no-st2", action="store_true", help="attention: stage 1 only (no sketch term)")
     a = ap.parse_args()
     import torch
     import iqsynth
@@ -54,8 +55,11 @@ def main():
             elif k == "quantize_qjl":
                 iq.iq_quantize_qjl(pq, x, codes, norms, qj, rn)
             elif k == "attention":
-                iq.iq_attention_scores(pq, codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk), qh,
-                                       qj[:H * nk].view(H, nk, -1), rn[:H * nk].view(H, nk))
+                if a.no_st2:
+                    iq.iq_attention_scores(pq, codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk), qh)
+                else:
+                    iq.iq_attention_scores(pq, codes[:H * nk].view(H, nk, -1), norms[:H * nk].view(H, nk), qh,
+                                           qj[:H * nk].view(H, nk, -1), rn[:H * nk].view(H, nk))
             else:
                 iq.iq_dequantize(p, codes, norms, y=y)
     torch.cuda.synchronize()
