@@ -751,7 +751,11 @@ def sweep(torch, iq, iqsynth, dev, stream, peak, steps: int = 20, settle_s: floa
                     fn = lambda i: iq.iq_roundtrip(p, xs[i & 1], y=ys[i & 1], stream=stream)
                     for i in range(3):
                         fn(i)
-                    t = sustained_time(torch, fn, steps, stream, settle_s) / steps
+                    # the settle, then the median of three back-to-back
+                    # windows (one window can catch a transient clock dip)
+                    ws = [sustained_time(torch, fn, steps, stream, settle_s if w == 0 else 0.0) / steps
+                          for w in range(3)]
+                    t = statistics.median(ws)
                     b = n * 2 * d * s
                     gbs = b / (t / 1e3) / 1e9
                     rows.append({"variant": vname, "dtype": dts, "d": d, "bits": bits, "us": 1e3 * t,
@@ -761,8 +765,8 @@ def sweep(torch, iq, iqsynth, dev, stream, peak, steps: int = 20, settle_s: floa
         torch.cuda.empty_cache()
     fp16 = [r["frac"] for r in rows if r["dtype"] == "f16"]
     return {"n": n, "kernel": "iq_roundtrip (fused, no code emission)", "rows": rows,
-            "timing": f"sustained: {settle_s} s untimed settle, then {steps} timed launches over 2 rotating "
-                      "buffer sets (CUDA events), per setting",
+            "timing": f"sustained: {settle_s} s untimed settle, then the median of three back-to-back windows "
+                      f"of {steps} timed launches over 2 rotating buffer sets (CUDA events), per setting",
             "min_frac": min(r["frac"] for r in rows), "min_frac_fp16": min(fp16)}
 
 
