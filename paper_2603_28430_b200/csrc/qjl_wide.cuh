@@ -22,9 +22,10 @@
 //                gamma^2 += r^2 (R23), r * 256 / max(rho, eps) split into
 //                fp16 hi + lo, stored as the chunk's UMMA A tiles (K-major,
 //                128-byte swizzle);
-//   MMAs       : issued by one thread of the LAST warp to finish the chunk
-//                (a shared-memory arrival counter), so no warp is parked
-//                on the tensor pipe: z (+)= A_hi S_k^T + A_lo S_k^T, M = 128
+//   MMAs       : d = 256: issued by one thread of the LAST warp to finish
+//                the chunk (a shared-memory arrival counter), so no warp is
+//                parked on the tensor pipe; d = 512 (tensor-bound): a
+//                dedicated MMA warp (and a TMA warp refilling the S ring): z (+)= A_hi S_k^T + A_lo S_k^T, M = 128
 //                rows, N = m (one or two N = 256 instructions per K-step),
 //                fp32 in TMEM; the same thread refills the S ring;
 //   epilogue   : tcgen05.ld, sign bits [z >= 0] packed LSB-first (R22).
@@ -50,7 +51,11 @@ struct WGeo {
   // from L2 through a two-stage ring refilled by a dedicated TMA warp (the
   // refill must not wait for a compute warp to reach a polling point)
   static constexpr bool RES = NKC * B_STAGE <= 128 * 1024;
-  static constexpr int CTA_THREADS = 32 * (NWC + (RES ? 0 : 1));
+  // streamed S also gets a dedicated MMA warp (d = 512, where the tensor
+  // pipe is the bottleneck and must never wait for a compute warp to reach
+  // its arrival: 1.85-1.95 ms vs 2.1 ms with the last-arriver issue)
+  static constexpr bool MMAW = !RES;
+  static constexpr int CTA_THREADS = 32 * (NWC + (RES ? 0 : 2));
   static constexpr int RB = D * BITS / 8;        // code bytes per row
   static constexpr int NB = RES ? NKC : 2;        // S stages
   static constexpr int A_TILE = TILE * 128;      // one fp16 operand chunk (hi or lo): 16 KB
@@ -103,7 +108,8 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
   uint64_t* a_empty = b_empty + NB;      // MMAs of the stage done (tcgen05.commit)
   uint64_t* acc_full = a_empty + NA;     // MMAs of the tile done (tcgen05.commit)
   uint64_t* acc_empty = acc_full + NACC; // epilogue read the accumulator (NWC arrivals)
-  uint32_t* arrivals = reinterpret_cast<uint32_t*>(acc_empty + NACC);   // [NA] warps done with the stage
+  uint64_t* a_full = acc_empty + NACC;   // [NA] compute warps -> MMA warp (MMAW only; NWC arrivals)
+  uint32_t* arrivals = reinterpret_cast<uint32_t*>(a_full + NA);   // [NA] warps done with the stage (no MMAW)
   uint32_t* tmem_slot = arrivals + NA;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -117,7 +123,7 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
   const int rot = W::RES ? 0 : (int)(blockIdx.x % NKC);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-    for (int s = 0; s < NA; ++s) { mbar_init(&a_empty[s], 1); arrivals[s] = 0; }
+    for (int s = 0; s < NA; ++s) { mbar_init(&a_empty[s], 1); mbar_init(&a_full[s], NWC); arrivals[s] = 0; }
     for (int b = 0; b < NACC; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], NWC); }
     fence_mbar_init();
     // the first NB chunks of S (all of it when resident)
@@ -174,6 +180,21 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
           mbar_arrive_expect_tx(&b_full[st], W::B_STAGE);
           bulk_g2s(b_ring + st * W::B_STAGE, s_img + (size_t)((u + rot) % NKC) * W::B_STAGE, W::B_STAGE,
                    &b_full[st], pol);
+        }
+      }
+    }
+  }
+  if constexpr (W::MMAW) {
+    if (warp == NWC + 1) {   // ------------------------------ streamed S: the MMA warp
+      if (lane == 0) {
+        uint32_t c = 0, j = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+          const uint32_t b = j % NACC;
+          mbar_wait_tc(&acc_empty[b], ((j / NACC) & 1) ^ 1);
+          for (int k = 0; k < NKC; ++k, ++c) {
+            mbar_wait_tc(&a_full[c % NA], (c / NA) & 1);
+            issue(c, k, b, k == NKC - 1);
+          }
         }
       }
     }
@@ -336,6 +357,11 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
     }
     fence_async_smem();       // generic-proxy A writes -> tensor-core (async proxy) reads
     __syncwarp();
+    if constexpr (W::MMAW) {
+      if (lane == 0) mbar_arrive(&a_full[sa]);
+      ++c;
+      return;
+    }
     // one accumulator: the previous tile's epilogue runs before this tile's
     // first chunk is handed over (its MMAs overwrite that accumulator)
     if (NACC == 1 && k == 0 && tprev >= 0) epilogue(j - 1, tprev);
@@ -373,11 +399,11 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
       // two accumulators: the previous tile's epilogue once this tile's
       // first NA chunks are handed over (its accumulator is not reused
       // before the next tile)
-      if (NACC == 2 && k == NA - 1 && tprev >= 0) epilogue(j - 1, tprev);
+      if ((NACC == 2 || W::MMAW) && k == NA - 1 && tprev >= 0) epilogue(j - 1, tprev);
       if (k + 2 < NKC) fetch(t, k + 2, f0);
       else fetch(t + gridDim.x, 0, f0);
       chunk(f1, k + 1);
-      if (NACC == 2 && k + 1 == NA - 1 && tprev >= 0) epilogue(j - 1, tprev);
+      if ((NACC == 2 || W::MMAW) && k + 1 == NA - 1 && tprev >= 0) epilogue(j - 1, tprev);
     }
     // gamma = ||r|| over the row's 8 pieces (lanes pc = 0..7 of the group)
     float2 gs = g2;
