@@ -128,11 +128,19 @@ iq_status iq_make_params(int d, int bits, int variant, uint64_t seed, int device
  * pipeline) switch sets per tile and need set_rows to be a multiple of 256
  * (else UNSUPPORTED); iq_append_kv and iq_attention_scores take any set_rows
  * (sets finer than 256 rows, e.g. one set per (layer, head) with one row per
- * set per decode step).  Not supported by the stage-2 sketch or the
- * distortion gradient (UNSUPPORTED / no sketch).
+ * set per decode step).  The stage-2 sketch takes sets through
+ * iq_make_params_qjl_sets; the distortion gradient does not (UNSUPPORTED).
  */
 iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows,
                               int device, iq_params** out);
+
+/* iq_make_params_sets plus the stage-2 sketch S (one S for every set, R20):
+ * iq_quantize_qjl then uses set (r / set_rows) % n_sets for row r (set_rows a
+ * multiple of 256, else UNSUPPORTED).  At d in {64, 128} the set-switching
+ * sketch kernel forms the residual in the input domain (r = x - x^ against
+ * S), since the rotated-domain operator S M^T would be per set. */
+iq_status iq_make_params_qjl_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows,
+                                  int device, iq_params** out);
 
 /* n_sets and set_rows of a handle (1 and 0 for a single-set handle). */
 iq_status iq_params_sets_info(const iq_params* p, int* n_sets, int64_t* set_rows);

@@ -24,7 +24,7 @@ __all__ = [
     "iq_rotation_param_count", "iq_version", "LIB_PATH",
     "iq_make_params_qjl", "iq_qjl_bytes_per_vector", "iq_export_qjl_matrix", "iq_quantize_qjl",
     "iq_attention_scores", "iq_make_params_explicit", "iq_distortion_grad", "iq_rot_grad_from_operator_grad",
-    "iq_make_params_sets", "iq_export_params_set", "iq_append_kv",
+    "iq_make_params_sets", "iq_make_params_qjl_sets", "iq_export_params_set", "iq_append_kv",
 ]
 
 FULL, FAST, PLANAR2D = 0, 1, 2
@@ -69,6 +69,8 @@ _sig = {
     "iq_distortion_grad": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "iq_rot_grad_from_operator_grad": (_c_int, [_c_vp, _c_vp, _c_sz, _c_vp, _c_sz]),
     "iq_make_params_sets": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_vp)]),
+    "iq_make_params_qjl_sets": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_int, _c_i64, _c_int,
+                                         ctypes.POINTER(_c_vp)]),
     "iq_params_sets_info": (_c_int, [_c_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_c_i64)]),
     "iq_export_params_set": (_c_int, [_c_vp, _c_int, _c_vp, _c_sz]),
     "iq_append_kv": (_c_int, [_c_vp, _c_int, _c_i64, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp]),
@@ -171,6 +173,18 @@ def iq_make_params_sets(d: int, bits: int, variant, seed: int, n_sets: int, set_
     h = ctypes.c_void_p()
     _check(lib.iq_make_params_sets(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
                                    int(n_sets), int(set_rows), int(device), ctypes.byref(h)), "iq_make_params_sets")
+    return Params(h.value, d, bits, variant, seed, device)
+
+
+def iq_make_params_qjl_sets(d: int, bits: int, variant, seed: int, n_sets: int, set_rows: int,
+                            device: int = 0) -> Params:
+    """iq_make_params_sets plus the stage-2 sketch (one S for every set)."""
+    if isinstance(variant, str):
+        variant = VARIANTS[variant.lower()]
+    h = ctypes.c_void_p()
+    _check(lib.iq_make_params_qjl_sets(int(d), int(bits), int(variant), ctypes.c_uint64(seed & (2**64 - 1)),
+                                       int(n_sets), int(set_rows), int(device), ctypes.byref(h)),
+           "iq_make_params_qjl_sets")
     return Params(h.value, d, bits, variant, seed, device)
 
 

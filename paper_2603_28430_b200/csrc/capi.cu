@@ -205,6 +205,13 @@ iq_status iq_make_params_sets(int d, int bits, int variant, uint64_t seed, int n
   return make_params_impl(d, bits, variant, seed, device, false, out, nullptr, n_sets, set_rows);
 }
 
+iq_status iq_make_params_qjl_sets(int d, int bits, int variant, uint64_t seed, int n_sets, int64_t set_rows,
+                                  int device, iq_params** out) {
+  if (n_sets < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "n_sets must be >= 1");
+  if (n_sets > 1 && set_rows < 1) return fail(IQ_ERR_INVALID_ARGUMENT, "set_rows must be >= 1");
+  return make_params_impl(d, bits, variant, seed, device, true, out, nullptr, n_sets, set_rows);
+}
+
 iq_status iq_params_sets_info(const iq_params* p, int* n_sets, int64_t* set_rows) {
   if (!p) return fail(IQ_ERR_INVALID_ARGUMENT, "params handle is NULL");
   if (n_sets) *n_sets = p->hp.n_sets;
@@ -328,6 +335,8 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
   if (s != IQ_OK) return s;
   if (!p->hp.has_qjl || !p->d_qjl)
     return fail(IQ_ERR_INVALID_ARGUMENT, "handle has no stage-2 sketch (use iq_make_params_qjl)");
+  s = check_batch_sets(p);
+  if (s != IQ_OK) return s;
   if (n == 0) return IQ_OK;
   if (!x || !codes || !norms || !qjl || !rnorms)
     return fail(IQ_ERR_INVALID_ARGUMENT, "x, codes, norms, qjl and rnorms are required");

@@ -23,7 +23,7 @@
 
 namespace iq {
 
-template <class T, int D, int BITS, int VAR>
+template <class T, int D, int BITS, int VAR, bool SETS = false>
 struct QGeo {
   using Gm = Geo<T, D, BITS, VAR, 2>;            // stage-1 lane geometry of the code-emitting kernels
 #ifndef IQ_QJL_ROTD
@@ -60,7 +60,9 @@ struct QGeo {
   static constexpr int NST = 2;
   // 16-bit rows: residual in the rotated domain, r' = T x - rho C[code]
   // (no inverse rotation), against S' = S M^T as fp16 hi + lo (3 MMA passes)
-  static constexpr bool ROTD = sizeof(T) == 2 && IQ_QJL_ROTD;
+  // (parameter sets [R31]: the direct form, whose B operand S is the same
+  // for every set; S' = S M^T would be per set)
+  static constexpr bool ROTD = !SETS && sizeof(T) == 2 && IQ_QJL_ROTD;
   static constexpr int A_BYTES = TILE * D * 2;   // one fp16 operand tile (hi or lo)
   static constexpr int S_BYTES = M * D * 2;
   static constexpr int B_BYTES = ROTD ? 2 * S_BYTES : S_BYTES;   // the B image(s) in shared memory
@@ -172,12 +174,12 @@ __device__ __forceinline__ void store_residual(uint8_t* a_hi, uint8_t* a_lo, uin
   }
 }
 
-template <class T, int D, int BITS, int VAR>
-__global__ void __launch_bounds__(QGeo<T, D, BITS, VAR>::CTA_THREADS, 1)
+template <class T, int D, int BITS, int VAR, bool SETS = false>
+__global__ void __launch_bounds__(QGeo<T, D, BITS, VAR, SETS>::CTA_THREADS, 1)
 k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* x,
                const uint8_t* __restrict__ s_img, uint8_t* __restrict__ codes, float* __restrict__ norms,
                uint8_t* __restrict__ qjl, float* __restrict__ rnorms) {
-  using Q = QGeo<T, D, BITS, VAR>;
+  using Q = QGeo<T, D, BITS, VAR, SETS>;
   using Gm = typename Q::Gm;
   constexpr int NWC = Q::NWC, TILE = Q::TILE, M = Q::M, U = Q::U, NST = Q::NST;
   constexpr int EPC = Gm::EPC, G = Gm::G, CPL = Gm::CPL, VPW = Gm::VPW;
@@ -317,7 +319,10 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
     int s = 0;
     uint32_t ph = 0, j = 0;
     int64_t tprev = -1;
+    int cur_set = 0;                                   // operators of set 0 are loaded
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      // parameter sets [R31]: this tile's operators (tiles never straddle sets)
+      if constexpr (SETS) switch_ops<Gm, NWC>(mat, cb, t * TILE, cur_set, sub, warp, lane, ops, P);
       mbar_wait_warp(&full[s], ph, lane);
       const uint8_t* st = smem + s * Q::STAGE;
       const int ss_ = s;

@@ -389,9 +389,25 @@ k_qjl_sketch(const float* __restrict__ mat, const KCodebook cb, int64_t n, const
   prefetch_tile(blockIdx.x);
   Raw f0, f1;
   fetch(blockIdx.x, 0, f0);
+  int cur_set = 0;                                       // the operators of set 0 are loaded
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
     const int64_t ra = t * TILE + rp, rb = ra + 64;
     prefetch_tile(t + gridDim.x);
+    // parameter sets [R31]: this tile's operators (tiles never straddle
+    // sets), rewritten between two compute-warp barriers
+    if (cb.n_sets > 1) {
+      const int set = (int)((t * TILE / cb.set_rows) % cb.n_sets);
+      if (set != cur_set) {
+        cur_set = set;
+        const float4* ms = reinterpret_cast<const float4*>(mat + (size_t)set * cb.set_stride);
+        asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // the old operators are no longer read
+        for (int i = tid; i < D / PW * NQ; i += NWC * 32) {
+          const int b = i / NQ, qq = i % NQ;
+          ops[((b % BPP) * NQ + qq) * (D / 8) + b / BPP] = __ldg(ms + i);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
+      }
+    }
 #pragma unroll 1
     for (int k = 0; k < NKC; k += 2) {               // ping-pong: the next item loads while this one computes
       fetch(t, k + 1, f1);

@@ -144,3 +144,48 @@ def test_qjl_errors():
         iq.iq_quantize_qjl(p, x)                       # no sketch in this handle
     with pytest.raises(iq.IQError):
         iq.iq_make_params_qjl(32, 3, iq.FULL, SEED, device=0)    # GPU sketch: d in {64, 128, 256, 512}
+
+
+@pytest.mark.parametrize("dt", [iq.F16, iq.F32])
+@pytest.mark.parametrize("variant", [iq.FULL, iq.FAST, iq.PLANAR2D])
+@pytest.mark.parametrize("d,bits", [(64, 2), (128, 3), (128, 4), (256, 3), (512, 2)])
+def test_qjl_sets(d, bits, variant, dt):
+    """Per-(layer, head) parameter sets with the stage-2 sketch [R31]: row r
+    uses set (r // set_rows) % n_sets, S is shared; codes and norms equal
+    iq_quantize with the same handle, and each set's rows pass the oracle
+    check built with that set's parameters (seed + s)."""
+    n_sets, set_rows = 3, 256
+    n = 2 * n_sets * set_rows + 37
+    X = iqsynth.unit_vectors(n, d, 61 + d + bits, NP[dt])
+    p = iq.iq_make_params_qjl_sets(d, bits, variant, SEED, n_sets, set_rows, device=0)
+    x = torch.from_numpy(X).cuda()
+    codes, norms, qjl, rn = iq.iq_quantize_qjl(p, x)
+    cq, nq = iq.iq_quantize(p, x)
+    torch.cuda.synchronize()
+    codes, norms, qjl, rn = (t.cpu().numpy() for t in (codes, norms, qjl, rn))
+    assert np.array_equal(codes, cq.cpu().numpy()) and np.array_equal(norms, nq.cpu().numpy())
+    set_of_row = (np.arange(n) // set_rows) % n_sets
+    S = _sketch(d)
+    for s in range(n_sets):
+        rows = set_of_row == s
+        po = O.make_params(d, bits, variant, SEED + s)
+        w = O.block_width(variant)
+        mpad = -(-d // w) * w
+        X64 = X[rows].astype(np.float64)
+        rho_o = np.sqrt(np.sum(X64 * X64, axis=1))
+        R = X64 - O.decode(O.unpack_codes(codes[rows], bits, mpad), rho_o, po)
+        g_o = np.linalg.norm(R, axis=1)
+        assert np.all(np.abs(rn[rows] - g_o) <= 2e-5 * g_o)
+        Z = R @ S.T
+        mism = Q.unpack_bits(qjl[rows], d) != (Z >= 0)
+        assert mism.mean() <= 1e-4
+        if mism.any():
+            scale = np.linalg.norm(S, axis=1)[None, :] * g_o[:, None]
+            assert np.all(np.abs(Z[mism]) <= 1e-5 * scale[mism])
+
+
+def test_qjl_sets_need_256_row_sets():
+    p = iq.iq_make_params_qjl_sets(128, 3, iq.FULL, SEED, 2, 128, device=0)
+    x = torch.zeros((512, 128), dtype=torch.float16, device="cuda")
+    with pytest.raises(iq.IQError):
+        iq.iq_quantize_qjl(p, x)
