@@ -276,7 +276,9 @@ iq_status iq_quantize_qjl(const iq_params* p, int dtype, int64_t n, const void* 
  * |error| <= ~1e-3 * rho_hk * ||q_hj|| (stage 1), see DESIGN.md.  d in
  * {64, 128, 256, 512} (d > 128: the key tile's operand is built and
  * accumulated in 128-coordinate chunks); the stage-2 term needs d in
- * {64, 128} (UNSUPPORTED otherwise).  Head h uses parameter set h % n_sets.
+ * {64, 128}, or d = 256 at bits <= 3 (UNSUPPORTED otherwise: the sketch
+ * operands of wider key tiles do not fit shared memory).  Head h uses
+ * parameter set h % n_sets.
  * codes, norms, qjl, rnorms 16-byte aligned; with heads > 1,
  * n_keys % 4 == 0 (else MISALIGNED).
  */

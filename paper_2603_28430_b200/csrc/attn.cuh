@@ -41,7 +41,9 @@ struct AGeo {
   // one TMEM accumulator), so d = 256 / 512 keys fit the same buffers
   static constexpr int KCH = D < 128 ? D : 128;
   static constexpr int KC = D / KCH;             // chunks per tile
-  static constexpr bool ST2OK = D <= 128;        // stage-2 term (the sketch kernel's widths)
+  // stage-2 term: d <= 128, and d = 256 at b <= 3 (the widest key tiles and
+  // pair tables leave no shared memory for the sketch operands beyond that)
+  static constexpr bool ST2OK = D <= 128 || (D == 256 && BITS <= 3);
   static constexpr int NPART = ST2OK ? 2 : 1;    // A parts per buffer: stage 1 [, stage 2]
   static constexpr int QB = ST2OK ? D / 8 : 0;   // sketch bytes per key
   // ring stage: codes [TILE][RB] | norms [TILE] | sketch [TILE][QB] | gammas [TILE]
@@ -52,7 +54,9 @@ struct AGeo {
   static constexpr int STAGE = (G_OFF + (ST2OK ? TILE * 4 : 0) + 127) / 128 * 128;
   static constexpr int A_BYTES = TILE * KCH * 2; // one fp16 A operand chunk
   static constexpr int B_BYTES = NQ * D * 2;     // one fp16 B tile (queries, all of K)
-  static constexpr int S_BYTES = 128 * D * 2;    // S as a 128-row A operand (staged in the A buffers)
+  static constexpr int MT = D <= 128 ? 1 : D / 128;   // 128-row tiles of S (m = d sketch rows)
+  static constexpr int S_TILE = 128 * D * 2;     // one of them as an A operand (rows >= m zero)
+  static constexpr int S_BYTES = MT * S_TILE;    // all of S, staged in the drained A buffers
   static constexpr int A_OFF = 0;                // [2 buffers][NPART]
   static constexpr int B_OFF = A_OFF + 2 * NPART * A_BYTES;
   static constexpr int QT_OFF = B_OFF + NPART * B_BYTES;   // sigma q as fp16 [NQ][D] (B of the S q MMA)
@@ -79,11 +83,12 @@ struct AGeo {
   static constexpr int W_PROD = NWD + NWE, W_MMA = NWD + NWE + 1;
   static constexpr int CTA_THREADS = 32 * (NWD + NWE + 2);
   static constexpr int CGROUPS = KCH / 32;       // 32-coordinate groups per key and chunk
-  static constexpr int TMEM_COLS = 256;          // [NACC][stage 1, stage 2] x NQ, + NQ for S q
+  static constexpr int TMEM_COLS = 256;          // [NACC][stage 1, stage 2] x NQ, + MT NQ for S q
   static constexpr int SQ_COL = 2 * NACC * NQ;
   static_assert(D == 64 || D == 128 || D == 256 || D == 512, "attention consumer: d in {64, 128, 256, 512}");
   static_assert(NST >= 3, "ring too shallow");
   static_assert(!ST2OK || S_BYTES <= 4 * A_BYTES, "S staging");
+  static_assert(SQ_COL + MT * NQ <= TMEM_COLS, "TMEM");
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -339,23 +344,28 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
           const uint32_t idesc = (1u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
           const uint32_t sa = smem_u32(a_base), qb = smem_u32(smem + A::QT_OFF);
 #pragma unroll
-          for (int s = 0; s < D / 16; ++s)
-            umma_f16(tmem + A::SQ_COL, umma_desc_sw128(sa + umma_kstep_off(s, 128)),
-                     umma_desc_sw128(qb + umma_kstep_off(s, NQ)), idesc, s != 0);
+          for (int mt = 0; mt < A::MT; ++mt)           // sketch rows 128 mt .. 128 mt + 127
+#pragma unroll
+            for (int s = 0; s < D / 16; ++s)
+              umma_f16(tmem + A::SQ_COL + mt * NQ, umma_desc_sw128(sa + mt * A::S_TILE + umma_kstep_off(s, 128)),
+                       umma_desc_sw128(qb + umma_kstep_off(s, NQ)), idesc, s != 0);
           umma_commit(sq_bar);
         }
         mbar_wait_tc(sq_bar, nprep & 1);
         tc_fence_after();
         if (warp < 4) {
-          uint32_t v[16];
-          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + A::SQ_COL, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const int i = 32 * warp + lane;
-          if (i < D) {
+#pragma unroll 1
+          for (int mt = 0; mt < A::MT; ++mt) {
+            uint32_t v[16];
+            tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + A::SQ_COL + mt * NQ, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int i = 128 * mt + 32 * warp + lane;
+            if (i < D) {
 #pragma unroll
-            for (int jq = 0; jq < NQ; ++jq)
-              *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
-                  __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
+              for (int jq = 0; jq < NQ; ++jq)
+                *reinterpret_cast<__half*>(b_base + A::B_BYTES + umma_sw128_off(jq, i, NQ)) =
+                    __float2half_rn(__uint_as_float(v[jq]) * 0.125f);
+            }
           }
         }
         tc_fence_before();
@@ -407,7 +417,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
       // every chunk's code words (BITS per 32-coordinate group) and sketch
       // words, contiguous in the stage (consecutive lanes read consecutive
       // words: no bank conflicts); the stage is released once they are in
-      uint32_t cw[KC][NG][BITS], sw[NG];
+      uint32_t cw[KC][NG][BITS], sw[KC][NG];
       float dep = 0.0f;
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
@@ -432,20 +442,23 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
         }
       }
 #pragma unroll
-      for (int gi = 0; gi < NG; ++gi) {
-        sw[gi] = 0u;
-        if (A::ST2OK && st2) {
-          const int g = threadIdx.x + gi * NWD * 32;
-          const int gr = g / CGROUPS, gs = g % CGROUPS;
-          const bool gv = g < TILE * CGROUPS && gr < nk;
-          if (full_tile && g < TILE * CGROUPS) {
-            sw[gi] = lds32(stg + A::Q_OFF + qoff[gi]);
-          } else {
-            const uint32_t off = (uint32_t)(gr * A::QB + gs * 4);
-            sw[gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
-                                                   : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * A::QB + off));
+      for (int kc = 0; kc < KC; ++kc) {
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+          sw[kc][gi] = 0u;
+          if (A::ST2OK && st2) {
+            const int g = threadIdx.x + gi * NWD * 32;
+            const int gr = g / CGROUPS, gs = kc * CGROUPS + g % CGROUPS;   // sketch word gs of the key
+            const bool gv = g < TILE * CGROUPS && gr < nk;
+            if (full_tile && g < TILE * CGROUPS) {
+              sw[kc][gi] = lds32(stg + A::Q_OFF + qoff[gi] + kc * CGROUPS * 4);
+            } else {
+              const uint32_t off = (uint32_t)(gr * A::QB + gs * 4);
+              sw[kc][gi] = !gv ? 0u : (off + 4 <= qb16) ? lds32(stg + A::Q_OFF + off)
+                                                       : __ldg(reinterpret_cast<const uint32_t*>(sketch + hrow0 * A::QB + off));
+            }
+            dep += __uint_as_float(sw[kc][gi] & 0x007FFFFFu);
           }
-          dep += __uint_as_float(sw[gi] & 0x007FFFFFu);
         }
       }
       // rho and gamma of the tile's keys for the side table
@@ -507,7 +520,7 @@ k_attn_scores(const float* __restrict__ mat, const KCodebook cb, int heads, int6
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int b0 = c8 * 8 + 4 * e;
-                const uint32_t f = b0 >= 8 ? (sw[gi] >> (b0 - 8)) : (sw[gi] << (8 - b0));
+                const uint32_t f = b0 >= 8 ? (sw[kc][gi] >> (b0 - 8)) : (sw[kc][gi] << (8 - b0));
                 const uint2 t2 = lds64_addr(((f & (15u << 8)) | st_lane) + st_base);
                 hw[2 * e] = t2.x;
                 hw[2 * e + 1] = t2.y;

@@ -370,8 +370,8 @@ iq_status iq_attention_scores(const iq_params* p, int q_dtype, int heads, int64_
   if (n_q < 1 || n_q > 16) return fail(IQ_ERR_INVALID_ARGUMENT, "n_q must be in [1, 16]");
   if ((qjl == nullptr) != (rnorms == nullptr))
     return fail(IQ_ERR_INVALID_ARGUMENT, "qjl and rnorms must be both NULL or both set");
-  if (qjl && p->hp.d > 128)
-    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 term of the consumer supports d in {64, 128}");
+  if (qjl && !(p->hp.d <= 128 || (p->hp.d == 256 && p->hp.bits <= 3)))
+    return fail(IQ_ERR_UNSUPPORTED, "the stage-2 term of the consumer supports d in {64, 128}, and 256 at bits <= 3");
   if (qjl && (!p->hp.has_qjl || !p->d_qjl_a))
     return fail(IQ_ERR_INVALID_ARGUMENT, "stage-2 scores need a handle with the sketch (iq_make_params_qjl)");
   if (n_keys == 0) return IQ_OK;

@@ -433,12 +433,18 @@ bool build_qjl(HostParams* hp, std::string* err) {
       for (int k = 0; k < d; ++k)
         std::memcpy(&hp->qjl_img[umma_sw128_off(i, k, m)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
   }
+  // S as the consumer's S q A operand: 128-row tiles (rows >= m zero), tile
+  // t holding sketch rows 128 t .. 128 t + 127 (d <= 256: the consumer's
+  // stage-2 widths)
   hp->qjl_img_a.clear();
-  if (qjl_fused(d)) {
-    hp->qjl_img_a.assign(static_cast<size_t>(128) * d * 2, 0);
+  if (d <= 256) {
+    const int mt = (m + 127) / 128;
+    const size_t tile = static_cast<size_t>(128) * d * 2;
+    hp->qjl_img_a.assign(mt * tile, 0);
     for (int i = 0; i < m; ++i)
       for (int k = 0; k < d; ++k)
-        std::memcpy(&hp->qjl_img_a[umma_sw128_off(i, k, 128)], &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
+        std::memcpy(&hp->qjl_img_a[(i / 128) * tile + umma_sw128_off(i % 128, k, 128)],
+                    &hp->qjl_half[static_cast<size_t>(i) * d + k], 2);
   }
   hp->qjl_img_rot.clear();
   if (qjl_fused(d)) {

@@ -94,12 +94,22 @@ def test_attn_wide_shapes_and_head_switches(n_keys):
     _run(256, 3, iq.FAST, iq.F16, heads=300, n_keys=128, n_q=4, stage2=False, seed=3)
 
 
-def test_attn_wide_stage2_unsupported():
-    p = iq.iq_make_params(256, 3, iq.FULL, SEED, device=0)
-    codes = torch.zeros((1, 8, 96), dtype=torch.uint8, device="cuda")
+@pytest.mark.parametrize("bits", [2, 3])
+@pytest.mark.parametrize("variant", [iq.FULL, iq.FAST, iq.PLANAR2D])
+def test_attn_stage2_d256(variant, bits):
+    """The stage-2 term at d = 256 (b <= 3): S q over two 128-row tiles of S,
+    the sketch-bit operand in two K-chunks; ragged keys, several heads."""
+    _run(256, bits, variant, iq.F16, heads=3, n_keys=300, n_q=5, stage2=True, seed=17 + bits)
+
+
+@pytest.mark.parametrize("d,bits", [(256, 4), (512, 2)])
+def test_attn_wide_stage2_unsupported(d, bits):
+    p = iq.iq_make_params(d, bits, iq.FULL, SEED, device=0)
+    cb = d * bits // 8
+    codes = torch.zeros((1, 8, cb), dtype=torch.uint8, device="cuda")
     norms = torch.zeros((1, 8), dtype=torch.float32, device="cuda")
-    qjl = torch.zeros((1, 8, 32), dtype=torch.uint8, device="cuda")
-    q = torch.zeros((1, 2, 256), dtype=torch.float16, device="cuda")
+    qjl = torch.zeros((1, 8, d // 8), dtype=torch.uint8, device="cuda")
+    q = torch.zeros((1, 2, d), dtype=torch.float16, device="cuda")
     with pytest.raises(iq.IQError):
         iq.iq_attention_scores(p, codes, norms, q, qjl, norms.clone())
 

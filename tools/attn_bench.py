@@ -20,7 +20,7 @@ def main():
     import torch, iqsynth
     import paper_2603_28430_b200 as iq
     n = a.heads * a.keys
-    st2 = a.d <= 128                      # the stage-2 sketch exists for d in {64, 128}
+    st2 = a.d <= 128 or (a.d == 256 and a.bits <= 3)   # the consumer's stage-2 widths
     mk = iq.iq_make_params_qjl if st2 else iq.iq_make_params
     p = mk(a.d, a.bits, iq.VARIANTS[a.variant], iqsynth.PARAMS_SEED, device=0)
     codes = torch.empty((n, p.code_bytes), dtype=torch.uint8, device="cuda")
