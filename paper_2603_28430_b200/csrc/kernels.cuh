@@ -66,6 +66,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_B3_ALU
 #define IQ_B3_ALU 1          // b = 3 fused value chain: FSETP + predicated FADD (else FSET + FFMA2)
 #endif
+#ifndef IQ_BYTE_CODES
+#define IQ_BYTE_CODES 1      // byte-aligned code pieces stored in place (else gathered into words by shuffles)
+#endif
 #ifndef IQ_GRID_PAIR
 #define IQ_GRID_PAIR 0       // b = 4 grid decision with the two rows' FFMAs packed as FFMA2 (measured slower)
 #endif
@@ -129,7 +132,8 @@ constexpr int pick_cpl() {
 }
 
 // Kernel kinds: 0 quantize (K1), 1 fused roundtrip (K3), 2 fused roundtrip +
-// codes, 3 dequantize (K2), 4 distortion gradient, 5 quantize-on-append (K1's
+// codes, 3 dequantize (K2), 4 distortion gradient, 6 the stage-2 sketch
+// kernel's encoder (K3+codes' geometry), 5 quantize-on-append (K1's
 // lane geometry, so it emits K1's codes and norms bit for bit; operators in
 // registers because every lane group may use a different parameter set).  Coordinates per lane (TPL), measured on B200
 // (DESIGN.md section 6): 16 for every encoder except the fp32 code-emitting
@@ -156,12 +160,20 @@ constexpr int pick_tpl() {
   return f16 ? 16 : 8;
 }
 // Where an encoder whose operators exceed 32 registers per lane keeps them
-// (measured): shared memory (16 compute warps) for fp16 except the b <= 2
-// fused kernel, and for the fp32 quantizer; registers (8 warps) otherwise.
+// (measured under the bench's sustained protocol):
+// registers (8 compute warps) for the 16-bit fused kernel at every b and the
+// 16-bit fused + codes kernel at b <= 3 -- at the board's power cap the
+// per-block operator re-reads from shared memory cost more clock than the
+// 16-warp latency hiding buys (b = 3: 0.75 -> 0.79 of peak, b = 4: 0.715 ->
+// 0.75 at d = 128 ... 512); shared memory (16 compute warps) for the other
+// 16-bit encoders and the fp32 quantizer; registers (8 warps) otherwise.
 template <class T, int BITS, int KIND>
 constexpr bool pick_ops_smem() {
-  if (!IQ_OPS_SMEM || KIND >= 3) return false;   // decoder, gradient, append: registers
-  if (sizeof(T) == 2) return !(KIND == 1 && BITS <= 2);
+  if (!IQ_OPS_SMEM || (KIND >= 3 && KIND <= 5)) return false;   // decoder, gradient, append: registers
+  // KIND 6: the stage-2 sketch kernel's stage-1 encoder (qjl.cuh), K3+codes'
+  // lane geometry with its operators kept in shared memory (its 8 / 16 warps
+  // also hold the residual tiles)
+  if (sizeof(T) == 2) return !(KIND == 1 || (KIND == 2 && BITS <= 3));
   return KIND == 0;
 }
 
@@ -725,6 +737,30 @@ __device__ __forceinline__ uint32_t gather_word(uint32_t bits, int sub, int vbas
   }
 }
 
+// Store a lane's B code bits (B % 8 == 0) at byte address p of the row: one
+// aligned store for 8 / 16 / 32 bits (p is B/8-aligned), an aligned 16-bit +
+// 8-bit pair for 24 bits (odd: p odd, the byte goes first).
+template <int B>
+__device__ __forceinline__ void store_piece(uint8_t* p, uint32_t w, int odd, bool ok) {
+  if constexpr (B == 8) {
+    if (ok) *p = (uint8_t)w;
+  } else if constexpr (B == 16) {
+    if (ok) *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
+  } else if constexpr (B == 32) {
+    if (ok) *reinterpret_cast<uint32_t*>(p) = w;
+  } else {
+    static_assert(B == 24, "byte-aligned code pieces");
+    uint8_t* const p16 = p + odd;
+    uint8_t* const p8 = p + (odd ? 0 : 2);
+    const uint16_t v16 = (uint16_t)(odd ? (w >> 8) : w);
+    const uint8_t v8 = (uint8_t)(odd ? w : (w >> 16));
+    if (ok) {
+      *reinterpret_cast<uint16_t*>(p16) = v16;
+      *p8 = v8;
+    }
+  }
+}
+
 // Load a lane's block operators: lane coordinate c*EPC + e is global
 // coordinate (sub + c*G)*EPC + e; block b of the lane covers lane coordinates
 // b*PW .. b*PW+PW-1 (blocks never straddle a chunk since PW divides EPC).
@@ -1095,7 +1131,13 @@ k_encode(const float* __restrict__ mat, const KCodebook cb, int64_t n, const T* 
           if (oka) st_stream(yt + off, oa);
           if (okb) st_stream(yt + off + VPW * D, ob);
         }
-        if (emit) {
+        if constexpr (emit && IQ_BYTE_CODES && B % 8 == 0) {
+          // the lane's B code bits of chunk sub + i G are whole bytes of the
+          // row (LSB-first [R7]): store them in place, no gather shuffles
+          uint8_t* const pa = ct + vl * RB + (sub + i * G) * (B / 8);
+          store_piece<B>(pa, cwa[i], (sub + i * G) & 1, oka);
+          store_piece<B>(pa + VPW * RB, cwb[i], (sub + i * G) & 1, okb);
+        } else if constexpr (emit) {
           const uint32_t wa = gather_word<G, B>(cwa[i], sub, vbase);
           const uint32_t wb = gather_word<G, B>(cwb[i], sub, vbase);
           if (sub < W) {

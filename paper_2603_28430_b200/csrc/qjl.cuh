@@ -25,7 +25,7 @@ namespace iq {
 
 template <class T, int D, int BITS, int VAR, bool SETS = false>
 struct QGeo {
-  using Gm = Geo<T, D, BITS, VAR, 2>;            // stage-1 lane geometry of the code-emitting kernels
+  using Gm = Geo<T, D, BITS, VAR, 6>;            // stage-1 lane geometry of the code-emitting kernels
 #ifndef IQ_QJL_ROTD
 #define IQ_QJL_ROTD 1
 #endif

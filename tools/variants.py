@@ -59,6 +59,13 @@ VARIANTS = {
     "gridpair": ["-DIQ_GRID_PAIR=1"],       # b = 4 grid decision with the rows' FFMAs packed (FFMA2.RM / FFMA2)
     "fhadd": ["-DIQ_FHADD=1"],              # fp16 -> fp32 by FHADD (full-rate) instead of HADD2.F32
     "fhaddb3fma": ["-DIQ_FHADD=1", "-DIQ_B3_ALU=0"],
+    "opsreg_r64": ["-DIQ_OPS_SMEM=0", "-DIQ_RING_KB=64"],    # operators in registers, 64 / 128 / 160 KB ring
+    "opsreg_r128": ["-DIQ_OPS_SMEM=0", "-DIQ_RING_KB=128"],
+    "opsreg_r160": ["-DIQ_OPS_SMEM=0", "-DIQ_RING_KB=160"],
+    "opsreg_s16": ["-DIQ_OPS_SMEM=0", "-DIQ_STAGE_KB=16"],   # operators in registers, 16 / 64 KB stages
+    "opsreg_s64": ["-DIQ_OPS_SMEM=0", "-DIQ_STAGE_KB=64"],
+    "grid5": ["-DIQ_GRID_MIN_BITS=5"],      # b = 4 by the compare chain (no grid decision)
+    "wordcodes": ["-DIQ_BYTE_CODES=0"],     # code words gathered by shuffles (round-1/2 form) instead of byte pieces
 }
 
 
