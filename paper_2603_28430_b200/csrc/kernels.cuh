@@ -69,6 +69,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef IQ_BYTE_CODES
 #define IQ_BYTE_CODES 1      // byte-aligned code pieces stored in place (else gathered into words by shuffles)
 #endif
+#ifndef IQ_SIGN_SHF
+#define IQ_SIGN_SHF 0        // code sign bits by funnel shifts (else FSET + FFMA2 positional count)
+#endif
+#ifndef IQ_K1_OPS_REG
+#define IQ_K1_OPS_REG 1      // 16-bit quantizer at b = 3 with its operators in registers (8 compute warps; measured +5 %)
+#endif
 #ifndef IQ_GRID_PAIR
 #define IQ_GRID_PAIR 0       // b = 4 grid decision with the two rows' FFMAs packed as FFMA2 (measured slower)
 #endif
@@ -161,8 +167,9 @@ constexpr int pick_tpl() {
 }
 // Where an encoder whose operators exceed 32 registers per lane keeps them
 // (measured under the bench's sustained protocol):
-// registers (8 compute warps) for the 16-bit fused kernel at every b and the
-// 16-bit fused + codes kernel at b <= 3 -- at the board's power cap the
+// registers (8 compute warps) for the 16-bit fused kernel at every b, the
+// 16-bit fused + codes kernel at b <= 3 and the 16-bit quantizer at b = 3
+// (84.8 -> 80.7 us at d = 128) -- at the board's power cap the
 // per-block operator re-reads from shared memory cost more clock than the
 // 16-warp latency hiding buys (b = 3: 0.75 -> 0.79 of peak, b = 4: 0.715 ->
 // 0.75 at d = 128 ... 512); shared memory (16 compute warps) for the other
@@ -173,7 +180,7 @@ constexpr bool pick_ops_smem() {
   // KIND 6: the stage-2 sketch kernel's stage-1 encoder (qjl.cuh), K3+codes'
   // lane geometry with its operators kept in shared memory (its 8 / 16 warps
   // also hold the residual tiles)
-  if (sizeof(T) == 2) return !(KIND == 1 || (KIND == 2 && BITS <= 3));
+  if (sizeof(T) == 2) return !(KIND == 1 || (KIND == 2 && BITS <= 3) || (IQ_K1_OPS_REG && KIND == 0 && BITS == 3));
   return KIND == 0;
 }
 
@@ -640,15 +647,31 @@ __device__ __forceinline__ void encode_chunk(const float2* y, const RowQ<BITS>& 
     for (int i = 1; i < H; ++i)
       macc[e / A] = fma2(f2(ka >= q.thr[i].x ? 1.0f : 0.0f, kb >= q.thr[i].y ? 1.0f : 0.0f), bc(w),
                          macc[e / A]);
-    sacc[e / A] = fma2(f2(y[e].x < 0.0f ? 1.0f : 0.0f, y[e].y < 0.0f ? 1.0f : 0.0f), bc(w), sacc[e / A]);
+    if (!IQ_SIGN_SHF)
+      sacc[e / A] = fma2(f2(y[e].x < 0.0f ? 1.0f : 0.0f, y[e].y < 0.0f ? 1.0f : 0.0f), bc(w), sacc[e / A]);
   }
   uint32_t ma = 0, mb = 0, sa = 0, sb = 0;
 #pragma unroll
   for (int k = 0; k < NACC; ++k) {
     ma |= (__float_as_uint(macc[k].x) - 0x4B000000u) << (k * A * BITS);
     mb |= (__float_as_uint(macc[k].y) - 0x4B000000u) << (k * A * BITS);
-    sa |= (__float_as_uint(sacc[k].x) - 0x4B000000u) << (k * A * BITS);
-    sb |= (__float_as_uint(sacc[k].y) - 0x4B000000u) << (k * A * BITS);
+    if (!IQ_SIGN_SHF) {
+      sa |= (__float_as_uint(sacc[k].x) - 0x4B000000u) << (k * A * BITS);
+      sb |= (__float_as_uint(sacc[k].y) - 0x4B000000u) << (k * A * BITS);
+    }
+  }
+  if (IQ_SIGN_SHF) {
+    // sign bits funnelled in from the top, last coordinate first: group e
+    // ends with s_e in its top bit; shift it down to bit e * BITS and mask
+    uint32_t fa = 0, fb = 0, msk = 0;
+#pragma unroll
+    for (int e = EPC - 1; e >= 0; --e) {
+      fa = __funnelshift_l(__float_as_uint(y[e].x), fa, BITS);
+      fb = __funnelshift_l(__float_as_uint(y[e].y), fb, BITS);
+      msk |= 1u << (e * BITS);
+    }
+    sa = (fa >> (BITS - 1)) & msk;
+    sb = (fb >> (BITS - 1)) & msk;
   }
   uint32_t c = 0;
 #pragma unroll
@@ -1219,8 +1242,12 @@ k_append(const float* __restrict__ mat, const KCodebook cb, int64_t n_rows, cons
   uint8_t* cr = codes + (rr * cap + pos) * RB;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const uint32_t w = gather_word<G, B>(cwa[i], sub, vbase);
-    if (store && sub < W) *reinterpret_cast<uint32_t*>(cr + 4 * (i * W + sub)) = w;
+    if constexpr (IQ_BYTE_CODES && B % 8 == 0) {
+      store_piece<B>(cr + (sub + i * G) * (B / 8), cwa[i], (sub + i * G) & 1, store);
+    } else {
+      const uint32_t w = gather_word<G, B>(cwa[i], sub, vbase);
+      if (store && sub < W) *reinterpret_cast<uint32_t*>(cr + 4 * (i * W + sub)) = w;
+    }
   }
   if (store && sub == 0) norms[rr * cap + pos] = rho.x;
 }

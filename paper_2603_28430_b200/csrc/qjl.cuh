@@ -418,12 +418,18 @@ k_quantize_qjl(const float* __restrict__ mat, const KCodebook cb, int64_t n, con
         // codes + norms (bit-identical to iq_quantize)
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-          const uint32_t wa = gather_word<G, B>(cwa[i], sub, vbase);
-          const uint32_t wb = gather_word<G, B>(cwb[i], sub, vbase);
-          if (sub < W) {
-            const int off = vl * RB + 4 * (i * W + sub);
-            if (oka) *reinterpret_cast<uint32_t*>(ct + off) = wa;
-            if (okb) *reinterpret_cast<uint32_t*>(ct + off + VPW * RB) = wb;
+          if constexpr (IQ_BYTE_CODES && B % 8 == 0) {   // whole bytes: stored in place (k_encode)
+            uint8_t* const pa = ct + vl * RB + (sub + i * G) * (B / 8);
+            store_piece<B>(pa, cwa[i], (sub + i * G) & 1, oka);
+            store_piece<B>(pa + VPW * RB, cwb[i], (sub + i * G) & 1, okb);
+          } else {
+            const uint32_t wa = gather_word<G, B>(cwa[i], sub, vbase);
+            const uint32_t wb = gather_word<G, B>(cwb[i], sub, vbase);
+            if (sub < W) {
+              const int off = vl * RB + 4 * (i * W + sub);
+              if (oka) *reinterpret_cast<uint32_t*>(ct + off) = wa;
+              if (okb) *reinterpret_cast<uint32_t*>(ct + off + VPW * RB) = wb;
+            }
           }
         }
         // ---- residual r = x - rho T^-1(C[code]) (R21) -- or r' = T r in the

@@ -66,6 +66,9 @@ VARIANTS = {
     "opsreg_s64": ["-DIQ_OPS_SMEM=0", "-DIQ_STAGE_KB=64"],
     "grid5": ["-DIQ_GRID_MIN_BITS=5"],      # b = 4 by the compare chain (no grid decision)
     "wordcodes": ["-DIQ_BYTE_CODES=0"],     # code words gathered by shuffles (round-1/2 form) instead of byte pieces
+    "signshf": ["-DIQ_SIGN_SHF=1"],         # code sign bits by funnel shifts
+    "k1reg": ["-DIQ_K1_OPS_REG=1"],         # 16-bit quantizer b >= 3: operators in registers, 8 warps
+    "k1regshf": ["-DIQ_K1_OPS_REG=1", "-DIQ_SIGN_SHF=1"],
 }
 
 
