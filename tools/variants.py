@@ -72,6 +72,7 @@ VARIANTS = {
     "tpl8b4": ["-DIQ_TPL_K3B4=8"],          # b = 4 fused kernel: 8 coordinates per lane
     "pu1nwc12": ["-DIQ_PAIR_UNROLL=1", "-DIQ_NWC_NARROW=12"],   # one row pair per iteration, 12 warps
     "attn12": ["-DIQ_ATTN_NWD=12"],         # 12 decoder warps in the attention consumer
+    "qjl16": ["-DIQ_QJL_NWC=16"],           # 16 compute warps in the stage-2 kernel
 }
 
 
