@@ -215,8 +215,9 @@ struct Geo {
   static constexpr int GR = clcm(2 * NWC * VPW, 4);
   // stage size (measured): 64 KB for the 16-bit quantizer at b >= 3, d >= 128
   // (2-5 % over 32 / 16 KB; worse at fp32 and b = 2), 32 KB for the other
-  // b = 3 encoders and the b = 4 fused kernel (more rows per warp per
-  // mbarrier round trip), else 16 KB
+  // b = 3 encoders, the b = 4 fused kernel and the b <= 2 fused kernels
+  // (more rows per warp per mbarrier round trip; b = 2 fp16 sustained: fused
+  // 95.7 -> 91.1 us, fused + codes 113.4 -> 104.2 us), else 16 KB
 #ifdef IQ_STAGE_KB
   static constexpr int STAGE_KB = ENC ? IQ_STAGE_KB : 16;
 #else
@@ -228,6 +229,7 @@ struct Geo {
   static constexpr int DEC_KB = IQ_DEC_STAGE_KB ? IQ_DEC_STAGE_KB : (BITS <= 3 ? 32 : 16);
   static constexpr int STAGE_KB = (KIND == 0 && sizeof(T) == 2 && BITS >= 3 && D >= 128) ? 64
                                   : (ENC && (BITS == 3 || (KIND == 1 && BITS == 4))) ? 32
+                                  : ((KIND == 1 || KIND == 2) && BITS <= 2) ? 32
                                   : ENC ? 16 : DEC_KB;
 #endif
   static constexpr int TV0 = (STAGE_KB * 1024 / ROWB) / GR * GR;

@@ -1,5 +1,6 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputest5.log 2>&1; echo rc=$? >> gpurun_out/gputest5.log
-tail -2 gpurun_out/gputest5.log
-python tools/attn_bench.py --d 64 --bits 3 --variant full --heads 256 2>&1 | tail -1
-python tools/attn_bench.py --d 128 --bits 3 --variant full --heads 256 2>&1 | tail -1
-python bench.py > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo bench rc=$?
+python -m pytest tests -m gpu -x -q > gpurun_out/gputest6.log 2>&1; echo rc=$? >> gpurun_out/gputest6.log
+tail -2 gpurun_out/gputest6.log
+for s in "--d 128 --bits 2" "--d 256 --bits 2" "--d 512 --bits 2" "--d 128 --bits 1"; do
+  echo "== $s"; python tools/variants.py time $s --dtype f16 --variant full --sustained 0.5 --kernels rt rte --only base stage16 base stage16
+done
+python bench.py > gpurun_out/bench6.json 2> gpurun_out/bench6.err; echo bench rc=$?

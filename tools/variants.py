@@ -73,6 +73,8 @@ VARIANTS = {
     "pu1nwc12": ["-DIQ_PAIR_UNROLL=1", "-DIQ_NWC_NARROW=12"],   # one row pair per iteration, 12 warps
     "attn12": ["-DIQ_ATTN_NWD=12"],         # 12 decoder warps in the attention consumer
     "qjl16": ["-DIQ_QJL_NWC=16"],           # 16 compute warps in the stage-2 kernel
+    "stage32": ["-DIQ_STAGE_KB=32"],        # 32 KB ring stages for every encoder
+    "ringn128": ["-DIQ_RING_KB=128"],       # 128 KB ring for the 8-warp (register-operator) encoders
 }
 
 
