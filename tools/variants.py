@@ -75,6 +75,9 @@ VARIANTS = {
     "qjl16": ["-DIQ_QJL_NWC=16"],           # 16 compute warps in the stage-2 kernel
     "stage32": ["-DIQ_STAGE_KB=32"],        # 32 KB ring stages for every encoder
     "ringn128": ["-DIQ_RING_KB=128"],       # 128 KB ring for the 8-warp (register-operator) encoders
+    "nwcn6": ["-DIQ_NWC_NARROW=6"],         # 6 compute warps in the register-operator encoders
+    "nwcn4": ["-DIQ_NWC_NARROW=4"],
+    "b3fmar": ["-DIQ_B3_ALU=0"],            # b = 3 chain as FSET + FFMA2 (register-operator build)
 }
 
 
